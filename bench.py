@@ -1,0 +1,292 @@
+"""Benchmark of the JGS2 runtime iteration on B200 (driver contract).
+
+A *step* is one JGS2 outer iteration (Jacobi sweep in corotated_cubature
+mode incl. rotation refresh, exact reduced collect, sampled corrections,
+local line search and the sweep-level backtracking guard), i.e. one
+``LocalSolver.outer_solve`` iteration (reference local_solver.py:697-716).
+``value`` = sweeps/s over all ranks with the state resident in HBM;
+``e2e`` = the same through the C-ABI host-buffer call (x, z in from pinned
+host memory, x, dx out, every step). ``--impl reference`` times the CPU
+oracle port of the reference (numpy/SciPy, oracle/) on a bounded sample.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3]
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_HBM = 6650.0
+
+
+def hbm_peak():
+    try:
+        return float(json.loads(PEAKS.read_text())["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index=0):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap,utilization.gpu")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in Path(self.f.name).read_text().splitlines() if r.strip()]
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                r = [c.strip() for c in r]
+                util = float(r[6]) if len(r) > 6 and r[6] not in ("", "[N/A]") else 100.0
+                if util > 0:
+                    sm.append(float(r[0]))
+                mx = float(r[1])
+                for k, n in enumerate(names):
+                    if r[2 + k].lower().startswith("active"):
+                        reasons.add(n)
+            except Exception:
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    return world, rank, local, dist
+
+
+def barrier(dist):
+    if dist is not None:
+        import torch
+        dist.barrier()
+        torch.cuda.synchronize()
+
+
+def max_over_ranks(dist, v):
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------- CPU oracle
+def cpu_sample(config, steps=3, budget_s=25.0):
+    """Time the CPU oracle port (oracle/jgs2_oracle.py) on a bounded sample
+    of the workload: the same scene construction scaled down to ~10K tets,
+    injected precompute, ``steps`` sweeps; returns seconds/sweep scaled
+    linearly in element count to the full workload (measured 84-89
+    us/tet/sweep is linear in ne)."""
+    from oracle import jgs2_oracle as orc
+    from paper_2506_06494_b200 import scenes
+    from paper_2506_06494_b200.precompute import Precompute
+    name = {"c3": "c3s4", "c1": "c1"}.get(config, "c3s4")
+    m, st, h, _ = scenes.build(name)
+    pre = Precompute.injected(m, h, samples=6, seed=0)
+    solver = orc.OracleSolver(m, pre, h, orc.OracleConfig(max_outer=steps))
+    times = []
+    t_all = time.perf_counter()
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        rot = orc.vertex_rotations(m, st.x)
+        solver.sweep(st, rot)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_all > budget_s:
+            break
+    per_sweep = statistics.median(times)
+    return per_sweep, m.num_elements, len(times), name
+
+
+def threads():
+    try:
+        import threadpoolctl
+        info = threadpoolctl.threadpool_info()
+        return max([i.get("num_threads", 1) for i in info] + [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--config", default=os.environ.get("JGS2_BENCH_CONFIG", "c3"))
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world, rank, local, dist = dist_setup()
+    metric = "JGS2 iterations/sec (sweeps/s) and ms per timestep to residual tol"
+
+    from paper_2506_06494_b200 import scenes
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        per, ne_s, n, name = cpu_sample(args.config, steps=max(args.steps, 1))
+        m_full, _, _, desc = scenes.build(args.config)
+        v = 1.0 / (per * m_full.num_elements / ne_s)
+        cores = threads()
+        line = {"impl": "reference", "metric": metric, "value": v, "unit": "sweeps/s",
+                "n_gpus": args.gpus, "steps": n, "warmup": 0,
+                "ms_per_step": 1e3 / v, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": desc, "parallelism": "1 CPU process"},
+                "cpu_baseline": {"value": v, "unit": "sweeps/s", "cores": cores, "kind": "port",
+                                 "sample": f"oracle port on {name} ({ne_s} tets, injected "
+                                           f"precompute), {n} sweeps, median s/sweep scaled "
+                                           f"linearly by element count to {m_full.num_elements}"},
+                "e2e": {"value": v, "unit": "sweeps/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    from paper_2506_06494_b200.local_solver import LocalSolver, SolverConfig
+    from paper_2506_06494_b200.precompute import Precompute
+    from paper_2506_06494_b200 import _lib as L
+    m, st, h, desc = scenes.build(args.config)
+    t0 = time.perf_counter()
+    pre = Precompute.injected(m, h, samples=6, seed=0)
+    t_pre = time.perf_counter() - t0
+    cfg = SolverConfig(max_outer=500)
+    solver = LocalSolver(m, cfg, precompute=pre, h_ref=h, device=local if world > 1 else 0)
+    fi = solver.factor_info
+    x_start = st.x.copy()
+    solver.set_state(st.x, st.z, h)
+    for _ in range(args.warmup):
+        solver.sweep_resident(True)
+    solver.set_state(x_start, st.z, h)
+    solver.phase_reset()
+    solver.profile(True)
+    launches0 = solver.kernel_launches
+    barrier(dist)
+    clocks = Clocks(local)
+    solver.timer_start()
+    for _ in range(args.steps):
+        solver.sweep_resident(True)
+    ms = solver.timer_stop()
+    clk = clocks.stop()
+    launches = solver.kernel_launches - launches0
+    ms = max_over_ranks(dist, ms)
+    phases = solver.phase_stats()
+    solver.profile(False)
+    value = world * args.steps / (ms / 1e3)
+
+    # roofline of the dominant phase (HBM-bound 3x3-block arithmetic + sparse solves)
+    peak, peak_kind = hbm_peak()
+    dom = max(phases, key=lambda p: phases[p][0])
+    d_ms, d_launch, d_bytes = phases[dom]
+    achieved = d_bytes / (d_ms / 1e3) / 1e9 if d_ms > 0 else 0.0
+    total_bytes = sum(p[2] for p in phases.values())
+
+    # end-to-end through the C ABI with pinned host buffers (x, z in; x, dx out)
+    nv = m.num_vertices
+    xin, o1 = L.pinned_array((nv, 3))
+    zin, o2 = L.pinned_array((nv, 3))
+    xout, o3 = L.pinned_array((nv, 3))
+    dxo, o4 = L.pinned_array((nv, 3))
+    xin[:] = x_start
+    zin[:] = st.z
+    inf = L.SweepInfo()
+    import ctypes
+    solver.timer_start()
+    for _ in range(args.e2e_steps):
+        L.check(solver._lib.jgs2_sweep_host(solver._ctx, L.ptr(xin, L.f64), L.ptr(zin, L.f64), h,
+                                            None, L.ptr(xout, L.f64), L.ptr(dxo, L.f64),
+                                            ctypes.byref(inf)), solver._ctx)
+        xin[:] = xout
+    e2e_ms = max_over_ranks(dist, solver.timer_stop())
+    e2e = world * args.e2e_steps / (e2e_ms / 1e3)
+
+    # one full timestep to the residual tolerance from the predictor
+    from paper_2506_06494_b200.model import SystemState
+    ts = SystemState(x=x_start.copy(), x_prev=st.x_prev.copy(), v=st.v.copy(), z=st.z.copy(), h=h)
+    solver.timer_start()
+    stats = solver.outer_solve(ts)
+    ts_ms = solver.timer_stop()
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        try:
+            per, ne_s, n, name = cpu_sample(args.config)
+            v = 1.0 / (per * m.num_elements / ne_s)
+            cpu = {"value": v, "unit": "sweeps/s", "cores": threads(), "kind": "port",
+                   "sample": f"oracle port on {name} ({ne_s} tets, injected precompute), {n} "
+                             f"sweeps, median s/sweep scaled linearly by element count to "
+                             f"{m.num_elements} tets"}
+        except Exception as exc:  # never fail the GPU line on the CPU sample
+            cpu = {"value": None, "unit": "sweeps/s", "cores": threads(), "kind": "port",
+                   "sample": f"failed: {exc}"}
+    if rank != 0:
+        return
+    line = {
+        "metric": metric, "value": value, "unit": "sweeps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": desc, "tets": m.num_elements, "vertices": nv,
+                   "precompute": "injected (structurally valid; Precompute.injected)",
+                   "cubature_samples": 6, "h": h, "parallelism": f"replicas x{world}",
+                   "l2": "inputs > L2 (factor %.2f GB)" % (8 * fi.nnz_dof / 1e9)},
+        "timestep": {"iterations": stats.outer_iterations, "converged": stats.converged,
+                     "ms": ts_ms},
+        "factor": {"nnz_L": int(fi.nnz_dof), "fronts": int(fi.nfronts), "levels": int(fi.nlevels),
+                   "max_front": int(fi.max_front), "ordering": "geometric nested dissection",
+                   "factor_s": round(solver.factor_seconds, 2), "precompute_s": round(t_pre, 2)},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "step_bytes": total_bytes / args.steps,
+                     "step_frac": (total_bytes / (ms / 1e3) / 1e9) / peak},
+        "phases_ms_per_step": {p: round(v[0] / args.steps, 4) for p, v in phases.items()},
+        "e2e": {"value": e2e, "unit": "sweeps/s", "h2d_bytes_per_step": 2 * 24 * nv,
+                "d2h_bytes_per_step": 2 * 24 * nv},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,205 @@
+/* jgs2.h -- C ABI of the B200-native JGS2 runtime iteration (sm_100a).
+ *
+ * Drop-in boundary for the reference package's hot path
+ *   tetsolve.local_solver.LocalSolver.sweep / .outer_solve
+ *   (/root/reference/pkg/src/tetsolve/local_solver.py:606-655, 688-721)
+ * in subspace="corotated_cubature", mode="jacobi".  The reference is pure
+ * Python with no FFI of its own; these entry points are what its
+ * LocalSolver would bind (see INTEGRATION.md for the ctypes stub).
+ *
+ * Conventions: plain pointers and sizes only; host arrays are caller-owned
+ * and copied; the context owns all device memory and one CUDA stream.
+ * Every call returns 0 on success or a negative JGS2_E* code; the message
+ * is available from jgs2_last_error().  No exceptions cross the ABI.
+ * FP64 values, int64 indices (numpy default), row-major 3x3 blocks.
+ * Deterministic: ordered gathers, no floating-point atomics.
+ */
+#ifndef JGS2_H
+#define JGS2_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define JGS2_OK 0
+#define JGS2_E_ARG -1        /* invalid argument / state (ValueError) */
+#define JGS2_E_CUDA -2       /* CUDA runtime / library failure */
+#define JGS2_E_FACTOR -3     /* rest Hessian not SPD (PrecomputeError) */
+#define JGS2_E_KEY -4        /* basis lacks rows of a cubature element (KeyError) */
+#define JGS2_E_INFEASIBLE -5 /* barrier distance <= 0 at the sweep start (FeasibilityError) */
+#define JGS2_E_NODEV -6      /* no CUDA device */
+
+typedef struct jgs2_ctx jgs2_ctx;
+
+/* Static scene data: the reference Model arrays (assembly.py:40-116). */
+typedef struct jgs2_model {
+  int64_t nv, ne;
+  const double* rest_positions; /* nv*3 (Hbar is built at rest, subspace.py:48-57) */
+  const int64_t* tets;          /* ne*4 */
+  const double* dm_inv;         /* ne*9 */
+  const double* volumes;        /* ne */
+  const double* mu;             /* ne */
+  const double* lam;            /* ne */
+  const double* elem_qmass;     /* ne  (rho V / 4, assembly.py:82-84) */
+  const double* masses;         /* nv */
+  const uint8_t* fixed_mask;    /* nv */
+  double norm_scale;            /* normalization.scale (assembly.py:112-116) */
+  /* contact (contact.py:216-240); n_planes/n_surface_* may be 0 */
+  int32_t has_barrier;
+  double dhat, kappa;
+  int64_t n_planes;
+  const double* plane_points;   /* n_planes*3 */
+  const double* plane_normals;  /* n_planes*3 (unit) */
+  int64_t n_bodies;
+  int64_t n_surface_vertices, n_surface_tris;
+  const int64_t* surface_vertices; /* ascending */
+  const int64_t* surface_tris;     /* n_surface_tris*3 */
+  const int64_t* vertex_body;      /* nv */
+  const int64_t* surface_tri_body; /* n_surface_tris */
+} jgs2_model;
+
+/* Precompute (harness.prepare, harness.py:57-107) in flat CSR form. */
+typedef struct jgs2_precompute {
+  int64_t n_bases, gmax;
+  const int64_t* vertices;   /* n_bases, ascending free vertex ids */
+  const double* gbar;        /* n_bases*9 */
+  const int64_t* group;      /* n_bases*gmax, -1 padded */
+  const double* gbar_rows;   /* n_bases*3*(3*gmax) row-major */
+  const int64_t* vrows_ptr;  /* n_bases+1 */
+  const int64_t* vrows_keys; /* retained vertex ids, ascending per basis */
+  const double* vrows;       /* nnz*9 */
+  const int64_t* cub_ptr;    /* n_bases+1 */
+  const int64_t* cub_elems;
+  const double* cub_weights;
+} jgs2_precompute;
+
+/* SolverConfig subset on the path (local_solver.py:38-56). */
+typedef struct jgs2_config {
+  double tol_dx;
+  int32_t max_outer;
+  int32_t local_line_search;
+  int32_t track_energy;
+  int32_t max_halvings;
+  double alpha_floor;
+} jgs2_config;
+
+/* sweep() info dict (local_solver.py:613-614, 654) + extras. */
+typedef struct jgs2_sweep_info {
+  int64_t line_search_activations;
+  double max_local_step;
+  double grad_norm;
+  double grad_sq;
+  double dx_norm;          /* normalization.scale * |dx| (assembly.py:118-120) */
+  double energy;           /* total_energy at the new x (track_energy) */
+  int32_t halvings;        /* global backtrack halvings */
+  int32_t n_pairs;         /* active pairs at the sweep start */
+} jgs2_sweep_info;
+
+typedef struct jgs2_factor_info {
+  int64_t n_free;          /* factored (free) vertices */
+  int64_t nnz_dof;         /* stored lower-triangular entries (DOF units) */
+  int64_t nfronts;
+  int64_t nlevels;
+  int64_t max_front;       /* largest front order (DOFs) */
+  double factor_seconds;
+} jgs2_factor_info;
+
+/* ---- lifecycle ------------------------------------------------------- */
+jgs2_ctx* jgs2_create(int32_t device);
+void jgs2_destroy(jgs2_ctx* ctx);
+const char* jgs2_last_error(const jgs2_ctx* ctx);
+int32_t jgs2_device_count(void);
+
+/* ---- setup (LocalSolver.__init__, local_solver.py:217-240) ------------ */
+int32_t jgs2_set_model(jgs2_ctx* ctx, const jgs2_model* model);
+int32_t jgs2_set_precompute(jgs2_ctx* ctx, const jgs2_precompute* pre, const jgs2_config* cfg);
+/* Rest Hessian M/h^2 + PSD elastic, Dirichlet-eliminated, factored on the
+ * device (replaces subspace.rest_factorization, subspace.py:126-130). */
+int32_t jgs2_factor_rest(jgs2_ctx* ctx, double h_ref, int32_t leaf_size, jgs2_factor_info* info);
+
+/* Factor a caller-supplied rest Hessian given as 3x3 blocks (row vertex,
+ * column vertex, row-major values) over the free vertices -- e.g. the very
+ * matrix the reference factored with SuperLU (harness.py:76-77). Blocks
+ * touching fixed vertices are ignored (their rows are identity). */
+int32_t jgs2_factor_blocks(jgs2_ctx* ctx, int64_t nblocks, const int64_t* brow, const int64_t* bcol,
+                           const double* bval, int32_t leaf_size, jgs2_factor_info* info);
+
+/* ---- state ----------------------------------------------------------- */
+int32_t jgs2_set_state(jgs2_ctx* ctx, const double* x, const double* z, double h);
+int32_t jgs2_set_x(jgs2_ctx* ctx, const double* x);
+int32_t jgs2_get_x(jgs2_ctx* ctx, double* x);
+int32_t jgs2_get_dx(jgs2_ctx* ctx, double* dx);
+int32_t jgs2_set_rotations(jgs2_ctx* ctx, const double* rotations /* nv*9 */);
+int32_t jgs2_get_rotations(jgs2_ctx* ctx, double* rotations);
+
+/* ---- hot path -------------------------------------------------------- */
+/* vertex_rotations(model, x) on the device state (subspace.py:206-231). */
+int32_t jgs2_rotations(jgs2_ctx* ctx);
+/* One Jacobi sweep on the device state (LocalSolver.sweep,
+ * local_solver.py:606-655). refresh_rotations != 0 recomputes the vertex
+ * rotations at x first, fused with the assembled-field pass (one
+ * outer_solve iteration, local_solver.py:699-703); 0 uses the context's
+ * current rotations. */
+int32_t jgs2_sweep(jgs2_ctx* ctx, int32_t refresh_rotations, jgs2_sweep_info* info);
+/* End-to-end sweep from HOST buffers: x, z in; x, dx out
+ * (h2d of x,z and d2h of x,dx inside the call). rotations may be NULL
+ * (then computed on device from x, as outer_solve does). */
+int32_t jgs2_sweep_host(jgs2_ctx* ctx, const double* x, const double* z, double h,
+                        const double* rotations, double* x_out, double* dx_out,
+                        jgs2_sweep_info* info);
+/* outer_solve (local_solver.py:688-721) on the device state. Per-iteration
+ * arrays have capacity max_outer; returns iterations in *iterations. */
+int32_t jgs2_outer_solve(jgs2_ctx* ctx, double* dx_norms, double* grad_norms, double* energies,
+                         double* max_local_steps, int64_t* activations, int32_t* iterations,
+                         int32_t* converged);
+
+/* ---- per-kernel entry points (parity tests; device state in/out) ------- */
+int32_t jgs2_total_energy(jgs2_ctx* ctx, const double* x, double* energy);
+int32_t jgs2_assembled_field(jgs2_ctx* ctx, double* g_asm /* nv*3 */);
+int32_t jgs2_reduced_collect(jgs2_ctx* ctx, const double* rotations, const double* g_asm,
+                             double* q /* nv*3 */);
+int32_t jgs2_sampled_corrections(jgs2_ctx* ctx, double* corr /* nv*9, free rows */);
+int32_t jgs2_reduced_systems(jgs2_ctx* ctx, double* a /* nv*9 */, double* g /* nv*3 */);
+/* Active pairs at the device x: rows of 10 doubles
+ * (kind, vertex, tri0, tri1, tri2, plane, d, bary0, bary1, bary2). */
+int32_t jgs2_find_pairs(jgs2_ctx* ctx, double* rows, int64_t capacity, int64_t* count);
+int32_t jgs2_last_kernel_launches(jgs2_ctx* ctx, int64_t* launches);
+
+/* ---- measurement ------------------------------------------------------ */
+#define JGS2_NPHASES 8
+/* phases: 0 vertex pass (rotations + assembled field), 1 collect rhs,
+ * 2 factor solve (forward + backward), 3 cubature element Hessians,
+ * 4 local systems + line search, 5 energy evaluations, 6 update/finalize,
+ * 7 contact (pairs, pair terms, caps). */
+int32_t jgs2_profile(jgs2_ctx* ctx, int32_t enable);
+/* accumulated device ms (CUDA events on the context stream), launch
+ * counts and algorithmic bytes per phase since the last reset */
+int32_t jgs2_phase_stats(jgs2_ctx* ctx, double* ms, int64_t* launches, double* bytes);
+int32_t jgs2_phase_reset(jgs2_ctx* ctx);
+/* CUDA-event stopwatch on the context stream */
+int32_t jgs2_timer_start(jgs2_ctx* ctx);
+int32_t jgs2_timer_stop(jgs2_ctx* ctx, double* ms);
+/* pinned host buffers for the end-to-end path */
+void* jgs2_pinned_alloc(int64_t bytes);
+void jgs2_pinned_free(void* p);
+/* feasibility_step_cap(model, x, dx) (assembly.py:263-291) on host arrays,
+ * for the frame driver's initialize_step (harness.py:130-134) */
+int32_t jgs2_step_cap(jgs2_ctx* ctx, const double* x, const double* dx, double* cap);
+
+/* ---- symbolic analysis (host only; no device needed) ------------------ */
+typedef struct jgs2_sym jgs2_sym;
+jgs2_sym* jgs2_sym_build(int64_t n, const int64_t* adj_ptr, const int32_t* adj,
+                         const double* coords, int32_t leaf_size);
+/* sizes[0]=nfronts, [1]=struct entries, [2]=nlevels, [3]=nnz_dof */
+int32_t jgs2_sym_sizes(const jgs2_sym* s, int64_t* sizes);
+int32_t jgs2_sym_export(const jgs2_sym* s, int32_t* perm, int32_t* parent, int32_t* col_begin,
+                        int32_t* col_end, int64_t* struct_ptr, int32_t* struct_pos,
+                        int32_t* level);
+void jgs2_sym_free(jgs2_sym* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* JGS2_H */

@@ -1,0 +1,71 @@
+"""Build the sm_100a shared library ``lib/libjgs2.so`` in-tree with nvcc.
+
+The library is the C-ABI boundary (``include/jgs2.h``). It links cuBLAS and
+cuSOLVER (used only by the one-time rest-Hessian factorization, never on the
+per-sweep path) and the static CUDA runtime.
+"""
+
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+CSRC = PKG / "csrc"
+LIBDIR = PKG / "lib"
+LIB = LIBDIR / "libjgs2.so"
+SOURCES = ["jgs2.cu", "symbolic.cpp"]
+HEADERS = ["context.cuh", "physics.cuh", "factor.cuh", "sweep.cuh", "contact.cuh",
+           "geometry.cuh", "symbolic.h"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nvcc():
+    cand = os.environ.get("NVCC") or shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    if not Path(cand).exists():
+        raise RuntimeError("nvcc not found; cannot build the sm_100a library")
+    return cand
+
+
+def cuda_lib_dir():
+    root = Path(nvcc()).resolve().parent.parent
+    for d in (root / "lib64", root / "targets" / "x86_64-linux" / "lib"):
+        if (d / "libcublas.so").exists() or (d / "libcublas.so.12").exists():
+            return d
+    return root / "lib64"
+
+
+def stale():
+    if not LIB.exists():
+        return True
+    t = LIB.stat().st_mtime
+    deps = [CSRC / s for s in SOURCES + HEADERS] + [PKG.parent / "include" / "jgs2.h"]
+    return any(p.exists() and p.stat().st_mtime > t for p in deps)
+
+
+def build(force=False, verbose=False):
+    if not force and not stale():
+        return LIB
+    LIBDIR.mkdir(exist_ok=True)
+    libdir = cuda_lib_dir()
+    tmp = LIB.with_suffix(".so.tmp")
+    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+           "-Xptxas", "-O3", "-I", str(PKG.parent / "include"),
+           *[str(CSRC / s) for s in SOURCES], "-o", str(tmp),
+           "-L", str(libdir), f"-Xlinker=-rpath,{libdir}", "-lcusolver", "-lcublas"]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+        print(" ".join(cmd))
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc failed:\n{res.stdout}\n{res.stderr}")
+    if verbose:
+        print(res.stderr)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(LIB)

@@ -1,0 +1,604 @@
+// IPC barrier path of the JGS2 sweep.
+// Reference: contact.py:142-284 (distances, derivatives, pair energies),
+// contact.py:162-240 (closest points + active-set detection),
+// assembly.py:263-291 (feasibility cap), local_solver.py:85-112, 418-470
+// (pair coupling rows, pair terms, alpha caps), energy.py:205-221 (barrier).
+//
+// Pair detection reproduces the reference's rounding order so the active
+// set is bit-exact: 3-term dots as (p0+p2)+p1 without FMA,
+// norms as sqrt((x^2+y^2)+z^2), region tests in the reference's order.
+#pragma once
+#include "context.cuh"
+#include "sweep.cuh"
+#include "geometry.cuh"
+
+namespace jgs2 {
+
+struct ContactDev {
+  int nsv, nst, nplanes;
+  double dhat, kappa;
+  const int* sv;
+  const int* st;
+  const int* vbody;
+  const int* tbody;
+  const double* planes;  // (point, normal) x nplanes
+};
+
+// Pass 1: per surface vertex, counts of plane hits (per plane) and
+// cross-body triangle hits (brute force over all surface triangles).
+__global__ void k_pair_count(ContactDev cd, const double* x, const double* dx, double gamma,
+                             int* cnt /* (nplanes+1) x nsv */) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cd.nsv) return;
+  int v = cd.sv[i];
+  double p[3];
+  load_pos(x, dx, gamma, v, p);
+  for (int pl = 0; pl < cd.nplanes; ++pl)
+    cnt[pl * cd.nsv + i] = (plane_dist(p, cd.planes + 6 * pl) < cd.dhat) ? 1 : 0;
+  int hits = 0;
+  int bv = cd.vbody[v];
+  for (int t = 0; t < cd.nst; ++t) {
+    if (cd.tbody[t] == bv) continue;
+    double a[3], b[3], c[3], bary[3];
+    load_pos(x, dx, gamma, cd.st[3 * t], a);
+    load_pos(x, dx, gamma, cd.st[3 * t + 1], b);
+    load_pos(x, dx, gamma, cd.st[3 * t + 2], c);
+    if (closest_point_tri(p, a, b, c, bary) < cd.dhat) ++hits;
+  }
+  cnt[cd.nplanes * cd.nsv + i] = hits;
+}
+
+// Single-block exclusive scan of n ints (in place into out), total at out[n].
+__global__ void k_scan_excl(const int* in, int* out, int n) {
+  __shared__ int warp_tot[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int base = 0; base < n; base += blockDim.x) {
+    int i = base + threadIdx.x;
+    int v = (i < n) ? in[i] : 0;
+    int s = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += t;
+    }
+    if (lane == 31) warp_tot[wid] = s;
+    __syncthreads();
+    if (wid == 0) {
+      int w = (lane < (int)(blockDim.x >> 5)) ? warp_tot[lane] : 0;
+      int ws = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, ws, o);
+        if (lane >= o) ws += t;
+      }
+      warp_tot[lane] = ws - w;
+    }
+    __syncthreads();
+    int excl = carry + warp_tot[wid] + s - v;
+    if (i < n) out[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[n] = carry;
+}
+
+// Pass 2: write pair rows in the reference order (contact.py:224-239).
+__global__ void k_pair_write(ContactDev cd, const double* x, const double* dx, double gamma,
+                             const int* off, int cap, double* rows, int* flag) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cd.nsv) return;
+  int v = cd.sv[i];
+  double p[3];
+  load_pos(x, dx, gamma, v, p);
+  for (int pl = 0; pl < cd.nplanes; ++pl) {
+    double d = plane_dist(p, cd.planes + 6 * pl);
+    if (d < cd.dhat) {
+      int o = off[pl * cd.nsv + i];
+      if (o < cap) {
+        double* r = rows + (size_t)kPairRow * o;
+        r[0] = 0; r[1] = v; r[2] = r[3] = r[4] = 0; r[5] = pl; r[6] = d; r[7] = r[8] = r[9] = 0.0;
+      }
+      if (d <= 0.0) atomicOr(flag, 1);
+    }
+  }
+  int o = off[cd.nplanes * cd.nsv + i];
+  int bv = cd.vbody[v];
+  for (int t = 0; t < cd.nst; ++t) {
+    if (cd.tbody[t] == bv) continue;
+    double a[3], b[3], c[3], bary[3];
+    load_pos(x, dx, gamma, cd.st[3 * t], a);
+    load_pos(x, dx, gamma, cd.st[3 * t + 1], b);
+    load_pos(x, dx, gamma, cd.st[3 * t + 2], c);
+    double d = closest_point_tri(p, a, b, c, bary);
+    if (d < cd.dhat) {
+      if (o < cap) {
+        double* r = rows + (size_t)kPairRow * o;
+        r[0] = 1; r[1] = v; r[2] = cd.st[3 * t]; r[3] = cd.st[3 * t + 1]; r[4] = cd.st[3 * t + 2];
+        r[5] = -1; r[6] = d; r[7] = bary[0]; r[8] = bary[1]; r[9] = bary[2];
+      }
+      if (d <= 0.0) atomicOr(flag, 1);
+      ++o;
+    }
+  }
+}
+
+// ------------------------------------------------ barrier + distance derivatives
+struct Barrier { double b, db, ddb; };
+// energy.py:205-221 (d <= 0 handled by the caller's feasibility flag)
+__device__ __forceinline__ Barrier barrier_fn(double d, double dhat, double kappa) {
+  Barrier r{0.0, 0.0, 0.0};
+  if (!(d > 0.0) || d >= dhat) return r;
+  double gap = d - dhat;
+  double ln = log(d / dhat);
+  r.b = -kappa * gap * gap * ln;
+  r.db = -kappa * (2.0 * gap * ln + gap * gap / d);
+  r.ddb = -kappa * (2.0 * ln + 4.0 * gap / d - gap * gap / (d * d));
+  return r;
+}
+
+__device__ __forceinline__ void skew3(const double* v, double* S) {
+  S[0] = 0.0; S[1] = -v[2]; S[2] = v[1];
+  S[3] = v[2]; S[4] = 0.0; S[5] = -v[0];
+  S[6] = -v[1]; S[7] = v[0]; S[8] = 0.0;
+}
+
+// Distance derivatives w.r.t. the 12 stencil DOFs (x, a, b, c) for a
+// triangle pair with frozen region (contact.py:51-159). g[12], H[144].
+__device__ double tri_pair_derivs(const double* X, const double* bary, double* g, double* H) {
+  for (int i = 0; i < 12; ++i) g[i] = 0.0;
+  for (int i = 0; i < 144; ++i) H[i] = 0.0;
+  int nz[3], cntnz = 0;
+  for (int k = 0; k < 3; ++k)
+    if (bary[k] != 0.0) nz[cntnz++] = k;
+  const double* x = X;
+  if (cntnz == 1) {  // point-point (contact.py:51-59)
+    int s = 1 + nz[0];
+    const double* y = X + 3 * s;
+    double r[3] = {x[0] - y[0], x[1] - y[1], x[2] - y[2]};
+    double d = norm3_np(r);
+    double u[3] = {r[0] / d, r[1] / d, r[2] / d};
+    for (int i = 0; i < 3; ++i) { g[i] = u[i]; g[3 * s + i] = -u[i]; }
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) {
+        double k = ((i == j ? 1.0 : 0.0) - u[i] * u[j]) / d;
+        H[12 * i + j] = k;
+        H[12 * i + 3 * s + j] = -k;
+        H[12 * (3 * s + i) + j] = -k;
+        H[12 * (3 * s + i) + 3 * s + j] = k;
+      }
+    return d;
+  }
+  if (cntnz == 2) {  // point-edge (contact.py:62-92), slots (0, 1+nz0, 1+nz1)
+    int sa = 1 + nz[0], sb = 1 + nz[1];
+    const double* a = X + 3 * sa;
+    const double* b = X + 3 * sb;
+    double w[3] = {x[0] - a[0], x[1] - a[1], x[2] - a[2]};
+    double e[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]};
+    double m[3];
+    cross3(w, e, m);
+    double r = norm3_np(m), el = norm3_np(e);
+    double d = r / el;
+    double mh[3] = {m[0] / r, m[1] / r, m[2] / r};
+    // sub-stencil DOFs (9): [x(0..2), a(3..5), b(6..8)]
+    double jw[27] = {0}, je[27] = {0}, jm[27];
+    for (int i = 0; i < 3; ++i) {
+      jw[9 * i + i] = 1.0; jw[9 * i + 3 + i] = -1.0;
+      je[9 * i + 3 + i] = -1.0; je[9 * i + 6 + i] = 1.0;
+    }
+    double Se[9], Sw[9];
+    skew3(e, Se); skew3(w, Sw);
+    for (int i = 0; i < 3; ++i)
+      for (int k = 0; k < 9; ++k) {
+        double s = 0.0;
+        for (int j = 0; j < 3; ++j) s += -Se[3 * i + j] * jw[9 * j + k] + Sw[3 * i + j] * je[9 * j + k];
+        jm[9 * i + k] = s;
+      }
+    double gm[3] = {mh[0] / el, mh[1] / el, mh[2] / el};
+    double el3 = el * el * el;
+    double ge[3] = {-(r / el3) * e[0], -(r / el3) * e[1], -(r / el3) * e[2]};
+    double gs[9];
+    for (int k = 0; k < 9; ++k) {
+      double s = 0.0;
+      for (int i = 0; i < 3; ++i) s += jm[9 * i + k] * gm[i] + je[9 * i + k] * ge[i];
+      gs[k] = s;
+    }
+    double bmm[9], bme[9], bee[9];
+    double el5 = el3 * el * el;
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) {
+        double I = (i == j) ? 1.0 : 0.0;
+        bmm[3 * i + j] = (I - mh[i] * mh[j]) / (r * el);
+        bme[3 * i + j] = -mh[i] * e[j] / el3;
+        bee[3 * i + j] = r * (3.0 * e[i] * e[j] / el5 - I / el3);
+      }
+    double Sg[9];
+    skew3(gm, Sg);
+    double hs[81];
+    for (int k = 0; k < 9; ++k)
+      for (int l = 0; l < 9; ++l) {
+        double s = 0.0;
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) {
+            s += jm[9 * i + k] * bmm[3 * i + j] * jm[9 * j + l];
+            s += jm[9 * i + k] * bme[3 * i + j] * je[9 * j + l];
+            s += je[9 * i + k] * bme[3 * j + i] * jm[9 * j + l];
+            s += je[9 * i + k] * bee[3 * i + j] * je[9 * j + l];
+            s += jw[9 * i + k] * (-Sg[3 * i + j]) * je[9 * j + l];
+            s += je[9 * i + k] * Sg[3 * i + j] * jw[9 * j + l];
+          }
+        hs[9 * k + l] = s;
+      }
+    int slots[3] = {0, sa, sb};
+    for (int bi = 0; bi < 3; ++bi)
+      for (int r2 = 0; r2 < 3; ++r2) {
+        g[3 * slots[bi] + r2] = gs[3 * bi + r2];
+        for (int bj = 0; bj < 3; ++bj)
+          for (int c2 = 0; c2 < 3; ++c2)
+            H[12 * (3 * slots[bi] + r2) + 3 * slots[bj] + c2] = hs[9 * (3 * bi + r2) + 3 * bj + c2];
+      }
+    return d;
+  }
+  // point-face (contact.py:95-127)
+  const double* a = X + 3;
+  const double* b = X + 6;
+  const double* c = X + 9;
+  double w[3] = {x[0] - a[0], x[1] - a[1], x[2] - a[2]};
+  double u[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]};
+  double v[3] = {c[0] - a[0], c[1] - a[1], c[2] - a[2]};
+  double n[3];
+  cross3(u, v, n);
+  double ln = norm3_np(n);
+  double nh[3] = {n[0] / ln, n[1] / ln, n[2] / ln};
+  double s = w[0] * nh[0] + w[1] * nh[1] + w[2] * nh[2];
+  double jw[36] = {0}, ju[36] = {0}, jv[36] = {0}, jn[36];
+  for (int i = 0; i < 3; ++i) {
+    jw[12 * i + i] = 1.0; jw[12 * i + 3 + i] = -1.0;
+    ju[12 * i + 3 + i] = -1.0; ju[12 * i + 6 + i] = 1.0;
+    jv[12 * i + 3 + i] = -1.0; jv[12 * i + 9 + i] = 1.0;
+  }
+  double Sv[9], Su[9];
+  skew3(v, Sv); skew3(u, Su);
+  for (int i = 0; i < 3; ++i)
+    for (int k = 0; k < 12; ++k) {
+      double t = 0.0;
+      for (int j = 0; j < 3; ++j) t += -Sv[3 * i + j] * ju[12 * j + k] + Su[3 * i + j] * jv[12 * j + k];
+      jn[12 * i + k] = t;
+    }
+  double gn[3] = {(w[0] - s * nh[0]) / ln, (w[1] - s * nh[1]) / ln, (w[2] - s * nh[2]) / ln};
+  for (int k = 0; k < 12; ++k) {
+    double t = 0.0;
+    for (int i = 0; i < 3; ++i) t += jw[12 * i + k] * nh[i] + jn[12 * i + k] * gn[i];
+    g[k] = t;
+  }
+  double pn[9], bnn[9];
+  double ln2 = ln * ln;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      double I = (i == j) ? 1.0 : 0.0;
+      pn[3 * i + j] = (I - nh[i] * nh[j]) / ln;
+      bnn[3 * i + j] = (-w[i] * nh[j] - nh[i] * w[j] - s * I + 3.0 * s * nh[i] * nh[j]) / ln2;
+    }
+  double Sg[9];
+  skew3(gn, Sg);
+  for (int k = 0; k < 12; ++k)
+    for (int l = 0; l < 12; ++l) {
+      double t = 0.0;
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+          t += jw[12 * i + k] * pn[3 * i + j] * jn[12 * j + l];
+          t += jn[12 * i + k] * pn[3 * i + j] * jw[12 * j + l];
+          t += jn[12 * i + k] * bnn[3 * i + j] * jn[12 * j + l];
+          t += ju[12 * i + k] * (-Sg[3 * i + j]) * jv[12 * j + l];
+          t += jv[12 * i + k] * Sg[3 * i + j] * ju[12 * j + l];
+        }
+      H[12 * k + l] = t;
+    }
+  double sign = (s >= 0.0) ? 1.0 : -1.0;
+  for (int k = 0; k < 12; ++k) g[k] *= sign;
+  for (int k = 0; k < 144; ++k) H[k] *= sign;
+  return fabs(s);
+}
+
+// Per pair: barrier energy, stencil gradient and PSD-projected Hessian
+// (contact.py:254-263 with project_spd=True).
+__global__ void k_pair_terms(int npairs, const double* rows, const double* x, const double* planes,
+                             double dhat, double kappa, double* pg, double* ph, double* pe) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= npairs) return;
+  const double* r = rows + (size_t)kPairRow * k;
+  double* g = pg + 12 * (size_t)k;
+  double* H = ph + 144 * (size_t)k;
+  if (r[0] == 0.0) {  // plane: d = (x - p).n, grad n, hess 0
+    const double* pl = planes + 6 * (int)r[5];
+    int v = (int)r[1];
+    double d = plane_dist(x + 3 * v, pl);
+    Barrier B = barrier_fn(d, dhat, kappa);
+    for (int i = 0; i < 12; ++i) g[i] = 0.0;
+    for (int i = 0; i < 144; ++i) H[i] = 0.0;
+    double h3[9];
+    for (int i = 0; i < 3; ++i) {
+      g[i] = B.db * pl[3 + i];
+      for (int j = 0; j < 3; ++j) h3[3 * i + j] = B.ddb * pl[3 + i] * pl[3 + j];
+    }
+    double V[9];
+    double a[9];
+    for (int i = 0; i < 9; ++i) a[i] = h3[i];
+    jacobi_eig<3>(a, V, 30);
+    double lam[3] = {fmax(a[0], 0.0), fmax(a[4], 0.0), fmax(a[8], 0.0)};
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) {
+        double s = 0.0;
+        for (int q = 0; q < 3; ++q) s += V[3 * i + q] * lam[q] * V[3 * j + q];
+        H[12 * i + j] = s;
+      }
+    pe[k] = B.b;
+    return;
+  }
+  double X[12];
+  for (int s = 0; s < 4; ++s) {
+    int w = (int)r[1 + s];
+    for (int c = 0; c < 3; ++c) X[3 * s + c] = x[3 * w + c];
+  }
+  double gd[12], Hd[144];
+  double d = tri_pair_derivs(X, r + 7, gd, Hd);
+  Barrier B = barrier_fn(d, dhat, kappa);
+  double a[144];
+  for (int i = 0; i < 12; ++i) {
+    g[i] = B.db * gd[i];
+    for (int j = 0; j < 12; ++j) a[12 * i + j] = B.ddb * gd[i] * gd[j] + B.db * Hd[12 * i + j];
+  }
+  for (int i = 0; i < 12; ++i)
+    for (int j = i + 1; j < 12; ++j) {
+      double s = 0.5 * (a[12 * i + j] + a[12 * j + i]);
+      a[12 * i + j] = a[12 * j + i] = s;
+    }
+  double V[144];
+  jacobi_eig<12>(a, V, 30);
+  double lam[12];
+  for (int i = 0; i < 12; ++i) lam[i] = fmax(a[13 * i], 0.0);
+  for (int i = 0; i < 12; ++i)
+    for (int j = 0; j < 12; ++j) {
+      double s = 0.0;
+      for (int q = 0; q < 12; ++q) s += V[12 * i + q] * lam[q] * V[12 * j + q];
+      H[12 * i + j] = s;
+    }
+  pe[k] = B.b;
+}
+
+// Vertex -> pair incidence: counts (pass 1) and ordered fill (pass 2, one
+// thread per vertex scanning the pair list: deterministic, pair order).
+__global__ void k_vp_count(int npairs, const double* rows, int* cnt) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= npairs) return;
+  const double* r = rows + (size_t)kPairRow * k;
+  int nm = (r[0] == 0.0) ? 1 : 4;
+  for (int s = 0; s < nm; ++s) atomicAdd(cnt + (int)r[1 + s], 1);
+}
+__global__ void k_vp_fill(int npairs, const double* rows, const int* ptr, int* fillpos, int* list) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= npairs) return;
+  const double* r = rows + (size_t)kPairRow * k;
+  int nm = (r[0] == 0.0) ? 1 : 4;
+  for (int s = 0; s < nm; ++s) {
+    int v = (int)r[1 + s];
+    int slot = atomicAdd(fillpos + v, 1);
+    list[ptr[v] + slot] = 4 * k + s;
+  }
+}
+// sort each vertex's short list by pair id (deterministic order)
+__global__ void k_vp_sort(int nv, const int* ptr, int* list) {
+  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  int a = ptr[v], b = ptr[v + 1];
+  for (int i = a + 1; i < b; ++i) {
+    int key = list[i], j = i - 1;
+    while (j >= a && list[j] > key) { list[j + 1] = list[j]; --j; }
+    list[j + 1] = key;
+  }
+}
+
+// g_asm[v] += pair gradient blocks (ascending pair order) (local_solver.py:319-322)
+__global__ void k_pair_grad_add(int nv, const int* ptr, const int* list, const double* pg, double* gasm) {
+  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  for (int q = ptr[v]; q < ptr[v + 1]; ++q) {
+    int k = list[q] >> 2, s = list[q] & 3;
+    for (int c = 0; c < 3; ++c) gasm[3 * v + c] += pg[12 * (size_t)k + 3 * s + c];
+  }
+}
+
+// barrier energy sum over the pair table (deterministic tree) into res[slot] += ...
+__global__ void k_pair_energy_sum(int npairs, const double* rows, double dhat, double kappa,
+                                  double* partials, unsigned* counter, double* out) {
+  double acc = 0.0;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < npairs; k += gridDim.x * blockDim.x) {
+    double d = rows[(size_t)kPairRow * k + 6];
+    acc += barrier_fn(d, dhat, kappa).b;
+  }
+  grid_reduce<OP_SUM>(acc, partials, counter, out);
+}
+__global__ void k_add_scalar(double* dst, const double* src) { *dst += *src; }
+
+// feasibility_step_cap (assembly.py:263-291): min over planes of d/rate
+// (moving surface vertices) and over all cross-body (sv, tri) of
+// dist / (|dx_v| + max |dx_tri|); returns 0.9 * min, capped at 1.
+__global__ void k_cap_planes(ContactDev cd, const double* x, const double* dx, double* partials,
+                             unsigned* counter, double* out) {
+  double mn = INFINITY;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cd.nsv * max(cd.nplanes, 1);
+       i += gridDim.x * blockDim.x) {
+    if (cd.nplanes == 0) break;
+    int pl = i / cd.nsv, j = i % cd.nsv;
+    int v = cd.sv[j];
+    const double* P = cd.planes + 6 * pl;
+    double d = plane_dist(x + 3 * v, P);
+    double rate = -__dadd_rn(__dadd_rn(__dmul_rn(dx[3 * v], P[3]), __dmul_rn(dx[3 * v + 1], P[4])),
+                             __dmul_rn(dx[3 * v + 2], P[5]));
+    if (rate > 0) mn = fmin(mn, d / rate);
+  }
+  grid_reduce<OP_MIN>(mn, partials, counter, out);
+}
+__global__ void k_cap_tris(ContactDev cd, const double* x, const double* dx, double* partials,
+                           unsigned* counter, double* out) {
+  double mn = INFINITY;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cd.nsv; i += gridDim.x * blockDim.x) {
+    int v = cd.sv[i];
+    double p[3] = {x[3 * v], x[3 * v + 1], x[3 * v + 2]};
+    double sp = norm3_np(dx + 3 * v);
+    int bv = cd.vbody[v];
+    for (int t = 0; t < cd.nst; ++t) {
+      if (cd.tbody[t] == bv) continue;
+      int a0 = cd.st[3 * t], a1 = cd.st[3 * t + 1], a2 = cd.st[3 * t + 2];
+      double st = fmax(fmax(norm3_np(dx + 3 * a0), norm3_np(dx + 3 * a1)), norm3_np(dx + 3 * a2));
+      double rate = sp + st;
+      if (!(rate > 1e-30)) continue;
+      double bary[3];
+      double d = closest_point_tri(p, x + 3 * a0, x + 3 * a1, x + 3 * a2, bary);
+      mn = fmin(mn, d / rate);
+    }
+  }
+  grid_reduce<OP_MIN>(mn, partials, counter, out);
+}
+
+// ------------------------------------------------------------------ host glue
+
+inline ContactDev contactdev(const Ctx& C) {
+  ContactDev cd;
+  cd.nsv = C.nsv; cd.nst = C.nst; cd.nplanes = C.nplanes; cd.dhat = C.dhat; cd.kappa = C.kappa;
+  cd.sv = C.sv; cd.st = C.st; cd.vbody = C.vbody; cd.tbody = C.tbody; cd.planes = C.planes;
+  return cd;
+}
+
+void contact_setup(Ctx& C, const jgs2_model* md) {
+  C.has_barrier = md->has_barrier != 0;
+  if (!C.has_barrier) return;
+  C.dhat = md->dhat;
+  C.kappa = md->kappa;
+  C.nplanes = (int)md->n_planes;
+  C.nbodies = (int)std::max<int64_t>(md->n_bodies, 1);
+  C.nsv = (int)md->n_surface_vertices;
+  C.nst = (int)md->n_surface_tris;
+  C.h_planes.assign(6 * (size_t)std::max(C.nplanes, 1), 0.0);
+  for (int p = 0; p < C.nplanes; ++p)
+    for (int c = 0; c < 3; ++c) {
+      C.h_planes[6 * p + c] = md->plane_points[3 * p + c];
+      C.h_planes[6 * p + 3 + c] = md->plane_normals[3 * p + c];
+    }
+  C.planes = C.upload(C.h_planes.data(), C.h_planes.size());
+  std::vector<int> sv(C.nsv), st(3 * (size_t)C.nst), vb(C.nv), tb(C.nst);
+  for (int i = 0; i < C.nsv; ++i) sv[i] = (int)md->surface_vertices[i];
+  for (size_t i = 0; i < st.size(); ++i) st[i] = (int)md->surface_tris[i];
+  for (int i = 0; i < C.nv; ++i) vb[i] = md->vertex_body ? (int)md->vertex_body[i] : 0;
+  for (int i = 0; i < C.nst; ++i) tb[i] = md->surface_tri_body ? (int)md->surface_tri_body[i] : 0;
+  C.sv = C.upload(sv.data(), sv.size());
+  C.st = C.upload(st.data(), st.size());
+  C.vbody = C.upload(vb.data(), vb.size());
+  C.tbody = C.upload(tb.data(), tb.size());
+  C.pair_count_sv = C.alloc<int>((size_t)(C.nplanes + 1) * C.nsv + 1);
+  C.vp_cnt = C.alloc<int>(C.nv + 1);
+  C.pair_off_sv = C.alloc<int>((size_t)(C.nplanes + 1) * C.nsv + 1);
+  C.vp_ptr = C.alloc<int>(C.nv + 1);
+  C.flag_d = C.alloc<int>(2);
+  C.npairs_d = C.alloc<int>(2);
+}
+
+void ensure_pair_capacity(Ctx& C, int64_t need) {
+  if (need <= C.cap_pairs) return;
+  int64_t cap = std::max<int64_t>(need * 2, 1024);
+  C.pairs = C.alloc<double>((size_t)cap * kPairRow);
+  C.pair_g = C.alloc<double>((size_t)cap * 12);
+  C.pair_h = C.alloc<double>((size_t)cap * 144);
+  C.pair_e = C.alloc<double>((size_t)cap);
+  C.vp_list = C.alloc<int>((size_t)cap * 4);
+  C.cap_pairs = cap;
+}
+
+// Detect active pairs at x + gamma*dx into the pair table; sets C.npairs
+// (host sync) and the infeasibility flag.
+void contact_find_pairs(Ctx& C, const double* x, const double* dx, double gamma) {
+  ContactDev cd = contactdev(C);
+  int n = (C.nplanes + 1) * C.nsv;
+  JGS2_CUDA(cudaMemsetAsync(C.flag_d, 0, sizeof(int), C.stream));
+  k_pair_count<<<grid_for(C.nsv, 128), 128, 0, C.stream>>>(cd, x, dx, gamma, C.pair_count_sv);
+  C.check_launch();
+  k_scan_excl<<<1, 1024, 0, C.stream>>>(C.pair_count_sv, C.pair_off_sv, n);
+  C.check_launch();
+  int total = 0;
+  JGS2_CUDA(cudaMemcpyAsync(&total, C.pair_off_sv + n, sizeof(int), cudaMemcpyDeviceToHost, C.stream));
+  C.sync();
+  ensure_pair_capacity(C, total);
+  k_pair_write<<<grid_for(C.nsv, 128), 128, 0, C.stream>>>(cd, x, dx, gamma, C.pair_off_sv,
+                                                           (int)C.cap_pairs, C.pairs, C.flag_d);
+  C.check_launch();
+  C.npairs = total;
+}
+
+bool contact_infeasible(Ctx& C) {
+  int f = 0;
+  JGS2_CUDA(cudaMemcpyAsync(&f, C.flag_d, sizeof(int), cudaMemcpyDeviceToHost, C.stream));
+  C.sync();
+  return f != 0;
+}
+
+// barrier energy of the current pair table added to res[slot]
+void contact_energy_at(Ctx& C, const double* dx, double gamma, int slot) {
+  contact_find_pairs(C, C.x, dx, gamma);
+  if (C.npairs == 0) return;
+  int s2 = R_AUX;
+  k_pair_energy_sum<<<std::min(grid_for(C.npairs), 64), kBlock, 0, C.stream>>>(
+      C.npairs, C.pairs, C.dhat, C.kappa, C.partials + s2 * kMaxPartials, C.counters + s2, C.res + s2);
+  C.check_launch();
+  k_add_scalar<<<1, 1, 0, C.stream>>>(C.res + slot, C.res + s2);
+  C.check_launch();
+}
+
+// Pair terms at the current x and vertex->pair incidence; adds pair
+// gradients into g_asm.
+void contact_add_gradients(Ctx& C) {
+  if (C.npairs == 0) return;
+  k_pair_terms<<<grid_for(C.npairs, 64), 64, 0, C.stream>>>(C.npairs, C.pairs, C.x, C.planes, C.dhat,
+                                                            C.kappa, C.pair_g, C.pair_h, C.pair_e);
+  C.check_launch();
+  JGS2_CUDA(cudaMemsetAsync(C.vp_cnt, 0, (C.nv + 1) * sizeof(int), C.stream));
+  k_vp_count<<<grid_for(C.npairs), kBlock, 0, C.stream>>>(C.npairs, C.pairs, C.vp_cnt);
+  C.check_launch();
+  k_scan_excl<<<1, 1024, 0, C.stream>>>(C.vp_cnt, C.vp_ptr, C.nv);
+  C.check_launch();
+  JGS2_CUDA(cudaMemsetAsync(C.vp_cnt, 0, (C.nv + 1) * sizeof(int), C.stream));
+  k_vp_fill<<<grid_for(C.npairs), kBlock, 0, C.stream>>>(C.npairs, C.pairs, C.vp_ptr, C.vp_cnt, C.vp_list);
+  C.check_launch();
+  k_vp_sort<<<grid_for(C.nv), kBlock, 0, C.stream>>>(C.nv, C.vp_ptr, C.vp_list);
+  C.check_launch();
+  k_pair_grad_add<<<grid_for(C.nv), kBlock, 0, C.stream>>>(C.nv, C.vp_ptr, C.vp_list, C.pair_g, C.gasm);
+  C.check_launch();
+}
+
+double contact_step_cap(Ctx& C, const double* x, const double* dx) {
+  ContactDev cd = contactdev(C);
+  double cap = 1.0;
+  if (C.nplanes > 0) {
+    k_cap_planes<<<red_grid(C.nsv * C.nplanes), kBlock, 0, C.stream>>>(
+        cd, x, dx, C.partials + R_CAP * kMaxPartials, C.counters + R_CAP, C.res + R_CAP);
+    C.check_launch();
+    double m = 0;
+    JGS2_CUDA(cudaMemcpyAsync(&m, C.res + R_CAP, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    C.sync();
+    if (std::isfinite(m)) cap = std::min(cap, 0.9 * m);
+  }
+  if (C.nbodies > 1 && C.nst > 0) {
+    k_cap_tris<<<red_grid(C.nsv), kBlock, 0, C.stream>>>(cd, x, dx, C.partials + R_CAP * kMaxPartials,
+                                                           C.counters + R_CAP, C.res + R_CAP);
+    C.check_launch();
+    double m = 0;
+    JGS2_CUDA(cudaMemcpyAsync(&m, C.res + R_CAP, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    C.sync();
+    if (std::isfinite(m)) cap = std::min(cap, 0.9 * m);
+  }
+  return std::max(cap, 0.0);
+}
+
+}  // namespace jgs2

@@ -1,0 +1,328 @@
+// Device context of one JGS2 solver instance (one GPU, one stream).
+#pragma once
+#include <cuda_runtime.h>
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "physics.cuh"
+#include "symbolic.h"
+
+namespace jgs2 {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define JGS2_CUDA(call)                                                                   \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      throw ::jgs2::Error(-2, std::string(#call) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+constexpr int kBlock = 256;
+constexpr int kMaxPartials = 4096;  // grid-reduction partial slots per reduction
+constexpr int kPairRow = 10;
+
+// Reduction result slots (device doubles), see Ctx::res.
+enum ResSlot {
+  R_ENERGY = 0,   // total energy of the last energy launch
+  R_GRADSQ,       // sum of g_asm^2 over free vertices
+  R_DX2,          // |dx|^2
+  R_DXMAX,        // max_v |dx_v|
+  R_CAP,          // feasibility cap (min)
+  R_EBEFORE,      // energy at the sweep start
+  R_AUX,          // scratch (barrier sum)
+  R_NSLOTS = 8
+};
+
+// Device-side factor of the free-vertex rest Hessian (supernodal, ND order).
+struct Factor {
+  bool ready = false;
+  Symbolic sym;
+  int nfree = 0;
+  int nfronts = 0, nlevels = 0;
+  int64_t nnz_alloc = 0;  // doubles in L storage
+  double* L = nullptr;
+  // per-front (device)
+  int* f_colbeg = nullptr;     // first DOF position
+  int* f_ns = nullptr;         // columns (DOF)
+  int* f_nr = nullptr;         // struct rows (DOF)
+  int64_t* f_loff = nullptr;   // panel offset in L (ld = ns + nr)
+  int64_t* f_uoff = nullptr;   // update-vector offset (nr entries)
+  int64_t* f_woff = nullptr;   // work-vector offset (nf entries)
+  int* f_cptr = nullptr;       // children CSR
+  int* f_clist = nullptr;
+  int64_t* f_sptr = nullptr;   // struct DOF list CSR (DOF units)
+  int* f_sdof = nullptr;       // global DOF positions of struct rows
+  int* f_rmap = nullptr;       // per front: struct row -> local index in parent (DOF)
+  int* level_fronts = nullptr; // fronts grouped by level
+  std::vector<int> level_ptr;  // host
+  std::vector<int> level_maxnf;
+  double* u = nullptr;         // update vectors
+  double* w = nullptr;         // work vectors (global fallback)
+  int max_nf = 0;
+  double seconds = 0.0;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int64_t launches = 0;
+
+  // sizes
+  int nv = 0, ne = 0, nfree = 0, smax = 0, gmax = 1, nuniq = 0;
+  int64_t nslots = 0;
+  bool have_model = false, have_pre = false;
+  double norm_scale = 1.0;
+  // config
+  double tol_dx = 1e-3, alpha_floor = 1e-6;
+  int max_outer = 500, max_halvings = 30;
+  bool local_line_search = true, track_energy = true;
+
+  // static device data
+  int4* tets = nullptr;
+  double* dminv = nullptr;     // ne*9
+  double4* eprops = nullptr;   // (vol, mu, lam, qmass)
+  int* inc_ptr = nullptr;      // nv+1
+  int* inc = nullptr;          // 4ne: e*4+slot, ascending e per vertex
+  double* mass = nullptr;
+  uint8_t* fixed = nullptr;
+  int* pos = nullptr;          // nv: factor position of a free vertex, -1 fixed
+  int* free_list = nullptr;    // nfree
+  double* rest = nullptr;      // nv*3
+  std::vector<double> h_rest;  // host copy for ND coordinates
+  std::vector<int64_t> h_tets;
+  std::vector<uint8_t> h_fixed;
+
+  // precompute (per vertex rows, zero for vertices without a basis)
+  double* gbar = nullptr;      // nv*9
+  int* group = nullptr;        // nv*gmax (vertex ids, -1 pad)
+  double* grows = nullptr;     // nv*3*3*gmax
+  int* cub_u = nullptr;        // nv*smax unique-element index, -1 invalid
+  double* cub_w = nullptr;     // nv*smax
+  double* cub_rows = nullptr;  // nv*smax*36
+  int4* cub_verts = nullptr;   // nv*smax
+  double* crest = nullptr;     // nv*9 rest constant C_v
+  int* uniq = nullptr;         // nuniq element ids
+  double* mplus = nullptr;     // nuniq*45 per-sweep projected reduced Hessians
+  // retained rows CSR for contact coupling rows (local_solver.py:85-112)
+  int* vr_ptr = nullptr;       // nv+1
+  int* vr_keys = nullptr;
+  double* vr_rows = nullptr;
+
+  // state
+  double h = 0.01;
+  double* x = nullptr;         // nv*3
+  double* z = nullptr;
+  double* R = nullptr;         // nv*9
+  double* gasm = nullptr;      // nv*3
+  double* b = nullptr;         // 3*nfree (rhs / solution, ND order)
+  double* delta = nullptr;     // nv*3
+  double* alpha0 = nullptr;    // nv
+  int* kacc = nullptr;         // nv accept iteration of the local search
+  double* dx = nullptr;        // nv*3
+  bool rot_valid = false;
+
+  // reductions
+  double* partials = nullptr;  // R_NSLOTS * kMaxPartials
+  unsigned* counters = nullptr;
+  double* res = nullptr;       // R_NSLOTS results (device)
+  double* h_res = nullptr;     // pinned mirror
+  // local line search bookkeeping
+  unsigned long long* ls_max = nullptr;  // (max_halvings+2) maxima of alpha0 over unaccepted (bits)
+  int* ls_cnt = nullptr;                  // (max_halvings+2) counts of unaccepted
+  int* ls_final = nullptr;                // [T, floor_flag]
+
+  // contact
+  bool has_barrier = false;
+  double dhat = 0, kappa = 0;
+  int nplanes = 0, nbodies = 1, nsv = 0, nst = 0;
+  double* planes = nullptr;    // nplanes*6 (point, normal)
+  std::vector<double> h_planes;
+  int* sv = nullptr;           // surface vertices
+  int* st = nullptr;           // surface tris *3
+  int* vbody = nullptr;        // nv
+  int* tbody = nullptr;        // nst
+  // pair table (device, capacity cap_pairs)
+  int64_t cap_pairs = 0;
+  double* pairs = nullptr;     // rows of kPairRow
+  int* npairs_d = nullptr;
+  int* pair_count_sv = nullptr;  // per surface vertex counts (plane+tri)
+  int* pair_off_sv = nullptr;
+  int npairs = 0;              // host copy for the current pair table
+  int* vp_cnt = nullptr;       // per-vertex pair counts (nv+1)
+  int* vp_ptr = nullptr;       // vertex -> pair incidence CSR (nv+1)
+  int* vp_list = nullptr;      // pair*4 + member slot
+  double* pair_g = nullptr;    // per pair 12 gradient
+  double* pair_h = nullptr;    // per pair 144 projected Hessian
+  double* pair_e = nullptr;    // per pair barrier energy
+  int* flag_d = nullptr;       // infeasibility flag
+
+  // measurement: per-phase CUDA-event intervals (accumulated at sync points)
+  bool profiling = false;
+  static constexpr int kPhases = 8;
+  double phase_ms[kPhases] = {0};
+  int64_t phase_launch[kPhases] = {0};
+  double phase_bytes[kPhases] = {0};
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  std::vector<cudaEvent_t> event_pool;
+  int cur_phase = -1;
+  int64_t launch_mark = 0;
+  cudaEvent_t cur_start = nullptr;
+  cudaEvent_t tstart = nullptr, tstop = nullptr;
+  cudaEvent_t take_event() {
+    if (event_pool.empty()) {
+      cudaEvent_t e;
+      JGS2_CUDA(cudaEventCreate(&e));
+      return e;
+    }
+    cudaEvent_t e = event_pool.back();
+    event_pool.pop_back();
+    return e;
+  }
+  void phase_begin(int p, double bytes) {
+    phase_bytes[p] += bytes;
+    if (!profiling) return;
+    cur_phase = p;
+    launch_mark = launches;
+    cur_start = take_event();
+    JGS2_CUDA(cudaEventRecord(cur_start, stream));
+  }
+  void phase_end() {
+    if (!profiling || cur_phase < 0) return;
+    cudaEvent_t stop = take_event();
+    JGS2_CUDA(cudaEventRecord(stop, stream));
+    phase_launch[cur_phase] += launches - launch_mark;
+    pending.push_back({cur_phase, {cur_start, stop}});
+    cur_phase = -1;
+  }
+  void collect_phases() {  // call after a stream sync
+    for (auto& p : pending) {
+      float ms = 0.f;
+      JGS2_CUDA(cudaEventElapsedTime(&ms, p.second.first, p.second.second));
+      phase_ms[p.first] += ms;
+      event_pool.push_back(p.second.first);
+      event_pool.push_back(p.second.second);
+    }
+    pending.clear();
+  }
+
+  Factor fac;
+  cublasHandle_t cublas = nullptr;
+  cusolverDnHandle_t cusolver = nullptr;
+
+  std::vector<void*> allocs;
+  template <class T>
+  T* alloc(size_t count) {
+    if (count == 0) count = 1;
+    void* p = nullptr;
+    JGS2_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    allocs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  template <class T>
+  T* upload(const T* host, size_t count) {
+    T* d = alloc<T>(count);
+    if (count) JGS2_CUDA(cudaMemcpyAsync(d, host, count * sizeof(T), cudaMemcpyHostToDevice, stream));
+    return d;
+  }
+  void sync() {
+    JGS2_CUDA(cudaStreamSynchronize(stream));
+    if (!pending.empty()) collect_phases();
+  }
+  void check_launch() {
+    ++launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw Error(-2, std::string("kernel launch: ") + cudaGetErrorString(e));
+  }
+  ~Ctx();
+};
+
+inline int grid_for(int64_t n, int block = kBlock) {
+  int64_t g = (n + block - 1) / block;
+  return (int)(g < 1 ? 1 : g);
+}
+// grid for grid-stride reductions (<= kMaxPartials blocks)
+inline int red_grid(int64_t n) { int g = grid_for(n); return g < 148 * 8 ? g : 148 * 8; }
+inline bool contact_active(const Ctx& C) { return C.has_barrier && C.nsv > 0; }
+
+// ------------------------------------------------------ deterministic reductions
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_down_sync(0xffffffffu, v, o));
+  return v;
+}
+
+enum RedOp { OP_SUM = 0, OP_MAX = 1, OP_MIN = 2 };
+
+template <int OP>
+__device__ __forceinline__ double red_combine(double a, double b) {
+  return OP == OP_SUM ? a + b : (OP == OP_MAX ? fmax(a, b) : fmin(a, b));
+}
+template <int OP>
+__device__ __forceinline__ double red_warp(double v) {
+  return OP == OP_SUM ? warp_sum(v) : (OP == OP_MAX ? warp_max(v) : warp_min(v));
+}
+
+// Block reduction (fixed tree), result valid in thread 0.
+template <int OP>
+__device__ double block_reduce(double v) {
+  __shared__ double sh[32];
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = red_warp<OP>(v);
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  int nw = (blockDim.x + 31) >> 5;
+  double ident = OP == OP_SUM ? 0.0 : (OP == OP_MAX ? -INFINITY : INFINITY);
+  v = (threadIdx.x < nw) ? sh[threadIdx.x] : ident;
+  if (wid == 0) v = red_warp<OP>(v);
+  return v;
+}
+
+// Single-pass grid reduction: every block deposits its partial; the last
+// block to finish combines all partials in block order (deterministic) and
+// writes res[slot]. gridDim.x must be <= kMaxPartials.
+template <int OP>
+__device__ void grid_reduce(double v, double* partials, unsigned* counter, double* out) {
+  double bsum = block_reduce<OP>(v);
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = bsum;
+    __threadfence();
+    unsigned t = atomicAdd(counter, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double ident = OP == OP_SUM ? 0.0 : (OP == OP_MAX ? -INFINITY : INFINITY);
+  double acc = ident;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x)
+    acc = red_combine<OP>(acc, ((volatile double*)partials)[i]);
+  acc = block_reduce<OP>(acc);
+  if (threadIdx.x == 0) {
+    *out = acc;
+    *counter = 0u;
+  }
+}
+
+}  // namespace jgs2

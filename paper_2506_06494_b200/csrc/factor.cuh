@@ -1,0 +1,507 @@
+// Rest-Hessian factor: assembly, multifrontal Cholesky and the per-sweep
+// supernodal forward/backward substitution of the exact reduced collect
+// (reference: local_solver.py:115-126 -> SciPy SuperLU.solve).
+//
+// Layout in HBM: all front panels live in one FP64 array L; front f owns a
+// column-major (nf x ns) panel at f_loff[f] with leading dimension
+// nf = ns + nr: rows [0, ns) are the dense diagonal block (lower triangle
+// used), rows [ns, nf) the off-diagonal rows (its row structure).
+#pragma once
+#include "context.cuh"
+
+#include <algorithm>
+#include <chrono>
+#include <map>
+
+namespace jgs2 {
+
+// ---------------------------------------------------------------- element Hessians
+// Projected reduced element Hessian (45 packed doubles, translation
+// complement coordinates) at positions xs (energy.py:169-189 +
+// project_psd, via the 9x9 complement).
+__device__ void element_mplus(const double* xs, const int4 t, const double* D, const double4 ep,
+                              double* out45) {
+  double x0[3], x1[3], x2[3], x3[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    x0[c] = xs[3 * t.x + c]; x1[c] = xs[3 * t.y + c];
+    x2[c] = xs[3 * t.z + c]; x3[c] = xs[3 * t.w + c];
+  }
+  double F[9];
+  deformation_gradient(x0, x1, x2, x3, D, F);
+  double M[81];
+  reduced_hessian9(F, D, ep.x, snh_const(ep.y, ep.z), M);
+  psd_project9(M);
+#pragma unroll 1
+  for (int i = 0; i < 9; ++i)
+    for (int j = 0; j <= i; ++j) out45[i * (i + 1) / 2 + j] = M[9 * i + j];
+}
+
+__global__ void k_element_mplus(int n, const int* elems, const double* xs, const int4* tets,
+                                const double* dminv, const double4* eprops, double* mplus) {
+  int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  int e = elems ? elems[u] : u;
+  double D[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) D[i] = dminv[9 * (size_t)e + i];
+  element_mplus(xs, tets[e], D, eprops[e], mplus + 45 * (size_t)u);
+}
+
+// Hbar BSR block (i, j) of free vertices: sum over elements containing both
+// (ascending element id) of the projected rest element block + mass term.
+__global__ void k_bsr_blocks(int nblocks, const int* brow, const int* bcol, const int* inc_ptr,
+                             const int* inc, const int4* tets, const double* mplus_all,
+                             const double* mass, double inv_h2, double* bval) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nblocks) return;
+  int i = brow[k], j = bcol[k];
+  double acc[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) acc[q] = 0.0;
+  for (int p = inc_ptr[i]; p < inc_ptr[i + 1]; ++p) {
+    int code = inc[p], e = code >> 2, si = code & 3;
+    int4 t = tets[e];
+    int sj = (t.x == j) ? 0 : (t.y == j) ? 1 : (t.z == j) ? 2 : (t.w == j) ? 3 : -1;
+    if (sj < 0) continue;
+    const double* M = mplus_all + 45 * (size_t)e;
+    // H12 block (si, sj) = sum_{p,q} U[si][p] M[(p r),(q s)] U[sj][q]
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        double v = 0.0;
+#pragma unroll
+        for (int pp = 0; pp < 3; ++pp)
+#pragma unroll
+          for (int qq = 0; qq < 3; ++qq)
+            v += kHad(si, pp) * M[tri9(3 * pp + r, 3 * qq + s)] * kHad(sj, qq);
+        acc[3 * r + s] += v;
+      }
+  }
+  if (i == j) {
+    double m = mass[i] * inv_h2;
+    acc[0] += m; acc[4] += m; acc[8] += m;
+  }
+#pragma unroll
+  for (int q = 0; q < 9; ++q) bval[9 * (size_t)k + q] = acc[q];
+}
+
+__global__ void k_scatter_orig(int nblocks, const int64_t* dst, const int* ld, const double* bval,
+                               double* L) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nblocks) return;
+  int64_t d = dst[k];
+  if (d < 0) return;
+  int l = ld[k];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) L[d + (int64_t)c * l + a] = bval[9 * (size_t)k + 3 * a + c];
+}
+
+// Extend-add of a child's update matrix (nr_c x nr_c, lower) into its parent.
+__global__ void k_extend_add(int nrc, const double* Uc, const int* rmap, int nsp, int nfp,
+                             double* Lp, int nrp, double* Up) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t tot = (int64_t)nrc * nrc;
+  if (idx >= tot) return;
+  int a = (int)(idx % nrc), bcol = (int)(idx / nrc);
+  if (a < bcol) return;
+  double v = Uc[idx];
+  int ra = rmap[a], rb = rmap[bcol];
+  if (rb < nsp) Lp[(int64_t)rb * nfp + ra] += v;
+  else Up[(int64_t)(rb - nsp) * nrp + (ra - nsp)] += v;
+}
+
+// ------------------------------------------------------------------ solve kernels
+constexpr int kSolveThreads = 256;
+constexpr int kSmemCapDoubles = 24576;  // 192 KB
+
+// Forward substitution L z = y for all fronts of one level (one CTA each).
+__global__ void __launch_bounds__(kSolveThreads)
+k_forward_level(const int* fronts, const int* colbeg, const int* f_ns, const int* f_nr,
+                const int64_t* loff, const int64_t* uoff, const int64_t* woff, const int* cptr,
+                const int* clist, const int64_t* sptr, const int* rmap, const double* L,
+                double* b, double* u, double* wglob) {
+  extern __shared__ double smem[];
+  int f = fronts[blockIdx.x];
+  int ns = f_ns[f], nr = f_nr[f], nf = ns + nr;
+  double* v = (nf <= kSmemCapDoubles) ? smem : (wglob + woff[f]);
+  const double* P = L + loff[f];
+  int cb = colbeg[f];
+  for (int i = threadIdx.x; i < nf; i += blockDim.x) v[i] = (i < ns) ? b[cb + i] : 0.0;
+  __syncthreads();
+  for (int k = cptr[f]; k < cptr[f + 1]; ++k) {
+    int c = clist[k];
+    int nrc = f_nr[c];
+    const int* rm = rmap + sptr[c];
+    const double* uc = u + uoff[c];
+    for (int i = threadIdx.x; i < nrc; i += blockDim.x) v[rm[i]] += uc[i];
+    __syncthreads();
+  }
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j0 = 0; j0 < ns; j0 += 32) {
+    int jb = min(32, ns - j0);
+    if (warp == 0) {
+      for (int jj = 0; jj < jb; ++jj) {
+        int j = j0 + jj;
+        double zj = v[j] / P[(int64_t)j * nf + j];
+        __syncwarp();
+        if (lane == jj) v[j] = zj;
+        if (lane > jj && lane < jb) v[j0 + lane] -= P[(int64_t)j * nf + j0 + lane] * zj;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int i = j0 + jb + threadIdx.x; i < nf; i += blockDim.x) {
+      double acc = 0.0;
+      for (int k = 0; k < jb; ++k) acc += P[(int64_t)(j0 + k) * nf + i] * v[j0 + k];
+      v[i] -= acc;
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < nf; i += blockDim.x) {
+    if (i < ns) b[cb + i] = v[i];
+    else u[uoff[f] + (i - ns)] = v[i];
+  }
+}
+
+// Backward substitution L^T x = z for all fronts of one level.
+__global__ void __launch_bounds__(kSolveThreads)
+k_backward_level(const int* fronts, const int* colbeg, const int* f_ns, const int* f_nr,
+                 const int64_t* loff, const int64_t* woff, const int64_t* sptr, const int* sdof,
+                 const double* L, double* b, double* wglob) {
+  extern __shared__ double smem[];
+  int f = fronts[blockIdx.x];
+  int ns = f_ns[f], nr = f_nr[f], nf = ns + nr;
+  if (ns == 0) return;
+  double* t = (nf <= kSmemCapDoubles) ? smem : (wglob + woff[f]);
+  double* xg = t + ns;
+  const double* P = L + loff[f];
+  int cb = colbeg[f];
+  const int* sd = sdof + sptr[f];
+  for (int i = threadIdx.x; i < nf; i += blockDim.x) t[i] = (i < ns) ? b[cb + i] : b[sd[i - ns]];
+  __syncthreads();
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (nr > 0) {
+    for (int j = warp; j < ns; j += nw) {
+      const double* col = P + (int64_t)j * nf + ns;
+      double acc = 0.0;
+      for (int k = lane; k < nr; k += 32) acc += col[k] * xg[k];
+      acc = warp_sum(acc);
+      if (lane == 0) t[j] -= acc;
+    }
+    __syncthreads();
+  }
+  for (int j1 = ns; j1 > 0; j1 -= 32) {
+    int j0 = max(0, j1 - 32);
+    if (j1 < ns) {
+      for (int j = j0 + warp; j < j1; j += nw) {
+        const double* col = P + (int64_t)j * nf;
+        double acc = 0.0;
+        for (int i = j1 + lane; i < ns; i += 32) acc += col[i] * t[i];
+        acc = warp_sum(acc);
+        if (lane == 0) t[j] -= acc;
+      }
+      __syncthreads();
+    }
+    if (warp == 0) {
+      for (int jj = j1 - 1; jj >= j0; --jj) {
+        double xj = t[jj] / P[(int64_t)jj * nf + jj];
+        __syncwarp();
+        int jr = j0 + lane;
+        if (jr < jj) t[jr] -= P[(int64_t)jr * nf + jj] * xj;
+        if (lane == 0) t[jj] = xj;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < ns; i += blockDim.x) b[cb + i] = t[i];
+}
+
+// ------------------------------------------------------------------ host side
+inline void factor_release(Ctx& C) { C.fac = Factor(); }
+
+struct BlockInput {
+  int64_t nblocks;
+  const int64_t* brow;
+  const int64_t* bcol;
+  const double* bval;
+};
+
+// Build the factor of the free-vertex rest Hessian on the device: either
+// assembled from the model at h_ref (blocks == nullptr) or from caller blocks.
+void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nullptr) {
+  auto t0 = std::chrono::steady_clock::now();
+  Factor& F = C.fac;
+  F = Factor();
+  const int nv = C.nv, ne = C.ne;
+  // ---- free-vertex graph (vertex adjacency through elements, incl. self)
+  std::vector<int> loc(nv, -1), glob;
+  for (int v = 0; v < nv; ++v)
+    if (!C.h_fixed[v]) { loc[v] = (int)glob.size(); glob.push_back(v); }
+  int n = (int)glob.size();
+  F.nfree = n;
+  std::vector<std::vector<int>> nb(n);
+  if (blocks) {
+    for (int64_t k = 0; k < blocks->nblocks; ++k) {
+      int64_t r = blocks->brow[k], c = blocks->bcol[k];
+      if (r < 0 || r >= nv || c < 0 || c >= nv) throw Error(-1, "block index out of range");
+      int lr = loc[r], lc = loc[c];
+      if (lr >= 0 && lc >= 0) { nb[lr].push_back(lc); nb[lc].push_back(lr); }
+    }
+  }
+  for (int e = 0; e < (blocks ? 0 : ne); ++e) {
+    const int64_t* t = &C.h_tets[4 * (size_t)e];
+    for (int a = 0; a < 4; ++a) {
+      int la = loc[t[a]];
+      if (la < 0) continue;
+      for (int c = 0; c < 4; ++c) {
+        int lc = loc[t[c]];
+        if (lc >= 0) nb[la].push_back(lc);
+      }
+    }
+  }
+  std::vector<int64_t> aptr(n + 1, 0);
+  std::vector<int32_t> adj;
+  for (int i = 0; i < n; ++i) {
+    auto& s = nb[i];
+    s.push_back(i);
+    std::sort(s.begin(), s.end());
+    s.erase(std::unique(s.begin(), s.end()), s.end());
+    aptr[i + 1] = aptr[i] + (int64_t)s.size();
+    adj.insert(adj.end(), s.begin(), s.end());
+  }
+  std::vector<double> coords(3 * (size_t)n);
+  for (int i = 0; i < n; ++i)
+    for (int c = 0; c < 3; ++c) coords[3 * (size_t)i + c] = C.h_rest[3 * (size_t)glob[i] + c];
+  build_symbolic(n, aptr.data(), adj.data(), coords.data(), leaf, F.sym);
+  Symbolic& S = F.sym;
+  F.nfronts = S.nfronts;
+  F.nlevels = S.nlevels;
+  const int NF = S.nfronts;
+  // ---- per-front metadata (DOF units)
+  std::vector<int> colbeg(NF), fns(NF), fnr(NF), cptr(S.child_ptr), clist(S.child_list);
+  std::vector<int64_t> loff(NF + 1, 0), uoff(NF + 1, 0), woff(NF + 1, 0), sptr(NF + 1, 0);
+  for (int f = 0; f < NF; ++f) {
+    colbeg[f] = 3 * S.col_begin[f];
+    fns[f] = 3 * (S.col_end[f] - S.col_begin[f]);
+    fnr[f] = 3 * (int)(S.struct_ptr[f + 1] - S.struct_ptr[f]);
+    int nf = fns[f] + fnr[f];
+    loff[f + 1] = loff[f] + (int64_t)nf * fns[f];
+    uoff[f + 1] = uoff[f] + fnr[f];
+    woff[f + 1] = woff[f] + nf;
+    sptr[f + 1] = sptr[f] + fnr[f];
+    F.max_nf = std::max(F.max_nf, nf);
+  }
+  F.nnz_alloc = loff[NF];
+  std::vector<int> sdof(sptr[NF]), rmap(sptr[NF], -1);
+  for (int f = 0; f < NF; ++f) {
+    int64_t o = sptr[f];
+    for (int64_t k = S.struct_ptr[f]; k < S.struct_ptr[f + 1]; ++k)
+      for (int c = 0; c < 3; ++c) sdof[o++] = 3 * S.struct_pos[k] + c;
+  }
+  for (int f = 0; f < NF; ++f) {
+    int p = S.parent[f];
+    if (p < 0) continue;
+    int pcb = S.col_begin[p], pce = S.col_end[p];
+    const int* ps = S.struct_pos.data() + S.struct_ptr[p];
+    int pn = (int)(S.struct_ptr[p + 1] - S.struct_ptr[p]);
+    int pns = 3 * (pce - pcb);
+    int64_t o = sptr[f];
+    for (int64_t k = S.struct_ptr[f]; k < S.struct_ptr[f + 1]; ++k) {
+      int q = S.struct_pos[k];
+      int locq;
+      if (q >= pcb && q < pce) locq = 3 * (q - pcb);
+      else {
+        const int* it = std::lower_bound(ps, ps + pn, q);
+        if (it == ps + pn || *it != q) throw Error(-1, "symbolic: child row missing from parent");
+        locq = pns + 3 * (int)(it - ps);
+      }
+      for (int c = 0; c < 3; ++c) rmap[o++] = locq + c;
+    }
+  }
+  // levels
+  F.level_ptr.assign(F.nlevels + 1, 0);
+  for (int f = 0; f < NF; ++f) F.level_ptr[S.level[f] + 1]++;
+  for (int l = 0; l < F.nlevels; ++l) F.level_ptr[l + 1] += F.level_ptr[l];
+  std::vector<int> lf(NF), fill(F.level_ptr.begin(), F.level_ptr.end() - 1);
+  for (int f = 0; f < NF; ++f) lf[fill[S.level[f]]++] = f;
+  F.level_maxnf.assign(F.nlevels, 0);
+  for (int f = 0; f < NF; ++f)
+    F.level_maxnf[S.level[f]] = std::max(F.level_maxnf[S.level[f]], fns[f] + fnr[f]);
+  // ---- device metadata
+  F.f_colbeg = C.upload(colbeg.data(), NF);
+  F.f_ns = C.upload(fns.data(), NF);
+  F.f_nr = C.upload(fnr.data(), NF);
+  F.f_loff = C.upload(loff.data(), NF + 1);
+  F.f_uoff = C.upload(uoff.data(), NF + 1);
+  F.f_woff = C.upload(woff.data(), NF + 1);
+  F.f_cptr = C.upload(cptr.data(), NF + 1);
+  F.f_clist = C.upload(clist.data(), clist.size());
+  F.f_sptr = C.upload(sptr.data(), NF + 1);
+  F.f_sdof = C.upload(sdof.data(), sdof.size());
+  F.f_rmap = C.upload(rmap.data(), rmap.size());
+  F.level_fronts = C.upload(lf.data(), NF);
+  F.u = C.alloc<double>(uoff[NF]);
+  F.w = C.alloc<double>(woff[NF]);
+  F.L = C.alloc<double>(F.nnz_alloc);
+  JGS2_CUDA(cudaMemsetAsync(F.L, 0, F.nnz_alloc * sizeof(double), C.stream));
+  // vertex -> position map for the sweep kernels
+  std::vector<int> pos(nv, -1), freel(n);
+  for (int i = 0; i < n; ++i) { pos[glob[i]] = S.iperm[i]; freel[i] = glob[i]; }
+  C.pos = C.upload(pos.data(), nv);
+
+  // ---- Hbar blocks (projected rest element Hessians, subspace.py:48-57)
+  double* mp_all = nullptr;
+  if (!blocks) {
+    JGS2_CUDA(cudaMallocAsync(&mp_all, 45 * (size_t)std::max(ne, 1) * sizeof(double), C.stream));
+    k_element_mplus<<<grid_for(ne, 128), 128, 0, C.stream>>>(ne, nullptr, C.rest, C.tets, C.dminv,
+                                                             C.eprops, mp_all);
+    C.check_launch();
+  }
+  int64_t nblocks = aptr[n];
+  std::vector<int> pfront(n, -1);
+  for (int f = 0; f < NF; ++f)
+    for (int p = S.col_begin[f]; p < S.col_end[f]; ++p) pfront[p] = f;
+  std::vector<int> brow(nblocks), bcol(nblocks), bld(nblocks);
+  std::vector<int64_t> bdst(nblocks, -1);
+  for (int i = 0; i < n; ++i) {
+    int pi = S.iperm[i];
+    for (int64_t k = aptr[i]; k < aptr[i + 1]; ++k) {
+      int j = adj[k];
+      brow[k] = glob[i];
+      bcol[k] = glob[j];
+      int pj = S.iperm[j];
+      if (pi < pj) continue;  // strictly upper in ND order
+      int f = pfront[pj];
+      int nf = fns[f] + fnr[f];
+      int lj = 3 * (pj - S.col_begin[f]);
+      int li;
+      if (pi < S.col_end[f]) li = 3 * (pi - S.col_begin[f]);
+      else {
+        const int* ps = S.struct_pos.data() + S.struct_ptr[f];
+        int pn = (int)(S.struct_ptr[f + 1] - S.struct_ptr[f]);
+        const int* it = std::lower_bound(ps, ps + pn, pi);
+        if (it == ps + pn || *it != pi) throw Error(-1, "symbolic: entry outside front structure");
+        li = fns[f] + 3 * (int)(it - ps);
+      }
+      bdst[k] = loff[f] + (int64_t)lj * nf + li;
+      bld[k] = nf;
+    }
+  }
+  int* d_brow = C.upload(brow.data(), nblocks);
+  int* d_bcol = C.upload(bcol.data(), nblocks);
+  int* d_bld = C.upload(bld.data(), nblocks);
+  int64_t* d_bdst = C.upload(bdst.data(), nblocks);
+  double* d_bval = C.alloc<double>(9 * (size_t)nblocks);
+  if (blocks) {
+    // caller values: sum duplicates per (row, col) in input order
+    std::map<std::pair<int, int>, int64_t> where;
+    for (int64_t k = 0; k < nblocks; ++k) where[{brow[k], bcol[k]}] = k;
+    std::vector<double> hv(9 * (size_t)nblocks, 0.0);
+    for (int64_t q = 0; q < blocks->nblocks; ++q) {
+      auto it = where.find({(int)blocks->brow[q], (int)blocks->bcol[q]});
+      if (it == where.end()) continue;  // touches a fixed vertex
+      for (int i = 0; i < 9; ++i) hv[9 * it->second + i] += blocks->bval[9 * q + i];
+    }
+    JGS2_CUDA(cudaMemcpyAsync(d_bval, hv.data(), hv.size() * sizeof(double), cudaMemcpyHostToDevice, C.stream));
+    C.sync();
+  } else {
+    k_bsr_blocks<<<grid_for(nblocks), kBlock, 0, C.stream>>>((int)nblocks, d_brow, d_bcol,
+                                                              C.inc_ptr, C.inc, C.tets, mp_all,
+                                                              C.mass, 1.0 / (h_ref * h_ref), d_bval);
+    C.check_launch();
+  }
+  k_scatter_orig<<<grid_for(nblocks), kBlock, 0, C.stream>>>((int)nblocks, d_bdst, d_bld, d_bval, F.L);
+  C.check_launch();
+  if (mp_all) JGS2_CUDA(cudaFreeAsync(mp_all, C.stream));
+
+  // ---- multifrontal numeric factorization in postorder
+  if (!C.cublas) {
+    if (cublasCreate(&C.cublas) != CUBLAS_STATUS_SUCCESS) throw Error(-2, "cublasCreate failed");
+    if (cusolverDnCreate(&C.cusolver) != CUSOLVER_STATUS_SUCCESS) throw Error(-2, "cusolverDnCreate failed");
+  }
+  cublasSetStream(C.cublas, C.stream);
+  cusolverDnSetStream(C.cusolver, C.stream);
+  int max_ns = 0;
+  for (int f = 0; f < NF; ++f) max_ns = std::max(max_ns, fns[f]);
+  int lwork = 0;
+  if (max_ns > 0 &&
+      cusolverDnDpotrf_bufferSize(C.cusolver, CUBLAS_FILL_MODE_LOWER, max_ns, F.L, max_ns + 1,
+                                  &lwork) != CUSOLVER_STATUS_SUCCESS)
+    throw Error(-2, "potrf buffer size");
+  double* work = C.alloc<double>(std::max(lwork, 1));
+  int* infos = C.alloc<int>(NF);
+  JGS2_CUDA(cudaMemsetAsync(infos, 0, NF * sizeof(int), C.stream));
+  std::vector<double*> Ubuf(NF, nullptr);
+  const double one = 1.0, mone = -1.0;
+  for (int f = 0; f < NF; ++f) {
+    int ns = fns[f], nr = fnr[f], nf = ns + nr;
+    double* Pf = F.L + loff[f];
+    if (nr > 0) {
+      JGS2_CUDA(cudaMallocAsync(&Ubuf[f], (size_t)nr * nr * sizeof(double), C.stream));
+      JGS2_CUDA(cudaMemsetAsync(Ubuf[f], 0, (size_t)nr * nr * sizeof(double), C.stream));
+    }
+    for (int k = cptr[f]; k < cptr[f + 1]; ++k) {
+      int c = clist[k];
+      int nrc = fnr[c];
+      if (nrc > 0) {
+        int64_t tot = (int64_t)nrc * nrc;
+        k_extend_add<<<grid_for(tot), kBlock, 0, C.stream>>>(nrc, Ubuf[c], F.f_rmap + sptr[c], ns,
+                                                             nf, Pf, nr, Ubuf[f]);
+        C.check_launch();
+        JGS2_CUDA(cudaFreeAsync(Ubuf[c], C.stream));
+        Ubuf[c] = nullptr;
+      }
+    }
+    if (ns > 0) {
+      if (cusolverDnDpotrf(C.cusolver, CUBLAS_FILL_MODE_LOWER, ns, Pf, nf, work, lwork, infos + f) !=
+          CUSOLVER_STATUS_SUCCESS)
+        throw Error(-2, "cusolverDnDpotrf failed");
+      if (nr > 0) {
+        if (cublasDtrsm(C.cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T,
+                        CUBLAS_DIAG_NON_UNIT, nr, ns, &one, Pf, nf, Pf + ns, nf) != CUBLAS_STATUS_SUCCESS)
+          throw Error(-2, "cublasDtrsm failed");
+        if (cublasDsyrk(C.cublas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, nr, ns, &mone, Pf + ns, nf,
+                        &one, Ubuf[f], nr) != CUBLAS_STATUS_SUCCESS)
+          throw Error(-2, "cublasDsyrk failed");
+      }
+    }
+  }
+  for (int f = 0; f < NF; ++f)
+    if (Ubuf[f]) JGS2_CUDA(cudaFreeAsync(Ubuf[f], C.stream));
+  std::vector<int> hinfo(NF);
+  JGS2_CUDA(cudaMemcpyAsync(hinfo.data(), infos, NF * sizeof(int), cudaMemcpyDeviceToHost, C.stream));
+  C.sync();
+  for (int f = 0; f < NF; ++f)
+    if (hinfo[f] != 0) throw Error(-3, "rest Hessian factorization failed: front " + std::to_string(f) +
+                                           " not positive definite (info " + std::to_string(hinfo[f]) + ")");
+  F.ready = true;
+  F.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// b <- Hbar_ff^{-1} b (ND-ordered DOFs): forward then backward level sweeps.
+void factor_solve(Ctx& C) {
+  Factor& F = C.fac;
+  for (int l = 0; l < F.nlevels; ++l) {
+    int cnt = F.level_ptr[l + 1] - F.level_ptr[l];
+    size_t sm = std::min(F.level_maxnf[l], kSmemCapDoubles) * sizeof(double);
+    k_forward_level<<<cnt, kSolveThreads, sm, C.stream>>>(
+        F.level_fronts + F.level_ptr[l], F.f_colbeg, F.f_ns, F.f_nr, F.f_loff, F.f_uoff, F.f_woff,
+        F.f_cptr, F.f_clist, F.f_sptr, F.f_rmap, F.L, C.b, F.u, F.w);
+    C.check_launch();
+  }
+  for (int l = F.nlevels - 1; l >= 0; --l) {
+    int cnt = F.level_ptr[l + 1] - F.level_ptr[l];
+    size_t sm = std::min(F.level_maxnf[l], kSmemCapDoubles) * sizeof(double);
+    k_backward_level<<<cnt, kSolveThreads, sm, C.stream>>>(
+        F.level_fronts + F.level_ptr[l], F.f_colbeg, F.f_ns, F.f_nr, F.f_loff, F.f_woff, F.f_sptr,
+        F.f_sdof, F.L, C.b, F.w);
+    C.check_launch();
+  }
+}
+
+}  // namespace jgs2

@@ -1,0 +1,827 @@
+// C-ABI implementation of the B200-native JGS2 runtime iteration.
+// See include/jgs2.h for the contract and DESIGN.md for the data layout.
+#include "../../include/jgs2.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+
+#include "context.cuh"
+#include "factor.cuh"
+#include "sweep.cuh"
+#include "contact.cuh"
+
+using namespace jgs2;
+
+jgs2::Ctx::~Ctx() {
+  if (stream) cudaStreamSynchronize(stream);
+  for (void* p : allocs) cudaFree(p);
+  if (h_res) cudaFreeHost(h_res);
+  for (auto& p : pending) { cudaEventDestroy(p.second.first); cudaEventDestroy(p.second.second); }
+  for (auto e : event_pool) cudaEventDestroy(e);
+  if (tstart) cudaEventDestroy(tstart);
+  if (tstop) cudaEventDestroy(tstop);
+  if (cublas) cublasDestroy(cublas);
+  if (cusolver) cusolverDnDestroy(cusolver);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+struct jgs2_ctx {
+  Ctx c;
+};
+struct jgs2_sym {
+  Symbolic s;
+};
+
+namespace {
+
+template <class F>
+int32_t guarded(jgs2_ctx* ctx, F&& fn) {
+  if (!ctx) return JGS2_E_ARG;
+  try {
+    ctx->c.err.clear();
+    JGS2_CUDA(cudaSetDevice(ctx->c.device));
+    fn(ctx->c);
+    return JGS2_OK;
+  } catch (const Error& e) {
+    ctx->c.err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    ctx->c.err = e.what();
+    return JGS2_E_ARG;
+  }
+}
+
+DevModel devmodel(const Ctx& C) {
+  DevModel m;
+  m.nv = C.nv; m.ne = C.ne; m.smax = C.smax; m.gmax = C.gmax; m.nfree = C.nfree;
+  m.tets = C.tets; m.dminv = C.dminv; m.eprops = C.eprops; m.inc_ptr = C.inc_ptr; m.inc = C.inc;
+  m.mass = C.mass; m.fixed = C.fixed; m.pos = C.pos; m.free_list = C.free_list;
+  return m;
+}
+
+LocalArgs localargs(Ctx& C) {
+  LocalArgs a;
+  memset(&a, 0, sizeof(a));
+  a.R = C.R; a.b = C.b; a.gbar = C.gbar; a.group = C.group; a.grows = C.grows;
+  a.cub_u = C.cub_u; a.cub_w = C.cub_w; a.cub_rows = C.cub_rows; a.cub_verts = C.cub_verts;
+  a.crest = C.crest; a.mplus = C.mplus; a.h = C.h;
+  a.delta = C.delta; a.alpha0 = C.alpha0; a.kacc = C.kacc;
+  a.line_search = C.local_line_search ? 1 : 0;
+  a.max_halvings = C.max_halvings;
+  a.ls_max = C.ls_max; a.ls_cnt = C.ls_cnt;
+  return a;
+}
+
+
+void require_ready(Ctx& C) {
+  if (!C.have_model) throw Error(JGS2_E_ARG, "model not set");
+  if (!C.have_pre) throw Error(JGS2_E_ARG, "precompute not set");
+  if (!C.fac.ready) throw Error(JGS2_E_ARG, "rest factor not built (jgs2_factor_rest)");
+}
+
+// ---- algorithmic bytes per phase: unique bytes a
+// phase must move at least once; re-reads served by L2 are not counted.
+double bytes_vertex(const Ctx& C) { return C.ne * (16.0 + 72 + 32 + 16) + C.nv * (24.0 + 24 + 8 + 72 + 24); }
+double bytes_rhs(const Ctx& C) { return C.nfree * (4.0 + 4 + 72 + 24 + 24); }
+double bytes_solve(const Ctx& C) { return 16.0 * (double)C.fac.sym.nnz_dof + 4.0 * 8 * 3 * C.nfree; }
+double bytes_cub(const Ctx& C) { return C.nuniq * (4.0 + 16 + 72 + 32 + 96 + 360); }
+double bytes_local(const Ctx& C) {
+  return C.nfree * (4.0 + 72 * 4 + 24 + 4 + 36 + 8 + 24) + C.nslots * (4.0 + 8 + 288 + 16) +
+         C.nuniq * 360.0 + C.nv * 72.0;
+}
+double bytes_energy(const Ctx& C, bool dx) { return C.ne * (16.0 + 72 + 32) + C.nv * (24.0 + 24 + 8 + (dx ? 24 : 0)); }
+double bytes_final(const Ctx& C) { return C.nv * (24.0 * 4) + C.nv * (24.0 + 8 + 4 + 24); }
+
+// Energy at x + gamma*dx (dx may be null) into res[slot]; includes the
+// barrier energies of the pairs active at that position.
+void launch_energy(Ctx& C, const double* dx, double gamma, int slot) {
+  DevModel m = devmodel(C);
+  int n = std::max(C.ne, C.nv);
+  C.phase_begin(5, bytes_energy(C, dx != nullptr));
+  k_energy<<<red_grid(n), kBlock, 0, C.stream>>>(m, C.x, dx, gamma, C.z, C.h,
+                                                  C.partials + slot * kMaxPartials,
+                                                  C.counters + slot, C.res + slot);
+  C.check_launch();
+  C.phase_end();
+  if (contact_active(C)) {
+    C.phase_begin(7, 0.0);
+    contact_energy_at(C, dx, gamma, slot);
+    C.phase_end();
+  }
+}
+
+void vertex_pass(Ctx& C, bool rot) {
+  DevModel m = devmodel(C);
+  C.phase_begin(0, bytes_vertex(C));
+  if (rot) k_vertex_pass<true><<<grid_for(C.nv), kBlock, 0, C.stream>>>(m, C.x, C.z, C.h, C.R, C.gasm);
+  else k_vertex_pass<false><<<grid_for(C.nv), kBlock, 0, C.stream>>>(m, C.x, C.z, C.h, C.R, C.gasm);
+  C.check_launch();
+  C.phase_end();
+  if (rot) C.rot_valid = true;
+}
+
+void collect(Ctx& C) {
+  DevModel m = devmodel(C);
+  C.phase_begin(1, bytes_rhs(C));
+  k_rhs<<<red_grid(C.nfree), kBlock, 0, C.stream>>>(m, C.R, C.gasm, C.b,
+                                                     C.partials + R_GRADSQ * kMaxPartials,
+                                                     C.counters + R_GRADSQ, C.res + R_GRADSQ);
+  C.check_launch();
+  C.phase_end();
+  C.phase_begin(2, bytes_solve(C));
+  factor_solve(C);
+  C.phase_end();
+}
+
+void local_systems(Ctx& C, double* A_out, double* g_out, double* corr_out) {
+  DevModel m = devmodel(C);
+  if (C.nuniq > 0) {
+    C.phase_begin(3, bytes_cub(C));
+    k_element_mplus<<<grid_for(C.nuniq, 128), 128, 0, C.stream>>>(C.nuniq, C.uniq, C.x, C.tets,
+                                                                   C.dminv, C.eprops, C.mplus);
+    C.check_launch();
+    C.phase_end();
+  }
+  C.phase_begin(4, bytes_local(C));
+  JGS2_CUDA(cudaMemsetAsync(C.ls_cnt, 0, (C.max_halvings + 2) * sizeof(int), C.stream));
+  JGS2_CUDA(cudaMemsetAsync(C.ls_max, 0, (C.max_halvings + 2) * sizeof(unsigned long long), C.stream));
+  LocalArgs a = localargs(C);
+  a.A_out = A_out; a.g_out = g_out; a.corr_out = corr_out;
+  a.npairs = contact_active(C) ? C.npairs : 0;
+  a.x = C.x; a.pairs = C.pairs; a.pair_g = C.pair_g; a.pair_h = C.pair_h;
+  a.vp_ptr = C.vp_ptr; a.vp_list = C.vp_list; a.planes = C.planes;
+  a.vr_ptr = C.vr_ptr; a.vr_keys = C.vr_keys; a.vr_rows = C.vr_rows;
+  k_local<<<grid_for(C.nfree, 128), 128, 0, C.stream>>>(m, a);
+  C.check_launch();
+  C.phase_end();
+}
+
+// One sweep on the device state. rot: compute rotations at x (outer_solve);
+// otherwise use the context's current rotations.
+void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
+  require_ready(C);
+  if (!rot && !C.rot_valid) throw Error(JGS2_E_ARG, "rotations not set");
+  DevModel m = devmodel(C);
+  bool guard = C.local_line_search;
+  if (contact_active(C)) {  // pairs at x (local_solver.py:612)
+    C.phase_begin(7, 0.0);
+    contact_find_pairs(C, C.x, nullptr, 0.0);
+    C.phase_end();
+  }
+  if (guard) {
+    launch_energy(C, nullptr, 0.0, R_EBEFORE);
+    if (contact_active(C) && contact_infeasible(C))
+      throw Error(JGS2_E_INFEASIBLE, "barrier distance <= 0 at the sweep start");
+  }
+  vertex_pass(C, rot);
+  if (contact_active(C)) {
+    C.phase_begin(7, 0.0);
+    contact_add_gradients(C);
+    C.phase_end();
+  }
+  collect(C);
+  local_systems(C, nullptr, nullptr, nullptr);
+  C.phase_begin(6, bytes_final(C));
+  if (guard) {
+    k_ls_final<<<1, 1, 0, C.stream>>>(C.max_halvings, C.alpha_floor, C.ls_cnt, C.ls_max, C.ls_final);
+    C.check_launch();
+  }
+  k_apply_alpha<<<grid_for(C.nv), kBlock, 0, C.stream>>>(m, C.delta, C.alpha0, C.kacc, C.ls_final,
+                                                          guard ? 1 : 0, C.max_halvings,
+                                                          C.alpha_floor, C.dx);
+  C.check_launch();
+  C.phase_end();
+  double gamma = 1.0;
+  int halvings = 0;
+  bool have_trial_energy = false;
+  int pairs_at_start = C.npairs;
+  if (guard) {
+    // global backtracking (local_solver.py:555-577)
+    bool cap_needed = contact_active(C) && (C.npairs > 0 || C.nplanes > 0);
+    if (cap_needed) {
+      C.phase_begin(7, 0.0);
+      gamma = contact_step_cap(C, C.x, C.dx);
+      C.phase_end();
+    }
+    int acts_ls = 0;
+    JGS2_CUDA(cudaMemcpyAsync(C.h_res + R_NSLOTS, C.ls_final + 2, sizeof(int), cudaMemcpyDeviceToHost, C.stream));
+    while (halvings <= C.max_halvings) {
+      launch_energy(C, C.dx, gamma, R_ENERGY);
+      JGS2_CUDA(cudaMemcpyAsync(C.h_res, C.res, R_NSLOTS * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+      C.sync();
+      double e0 = C.h_res[R_EBEFORE], et = C.h_res[R_ENERGY];
+      if (contact_active(C) && contact_infeasible(C)) et = INFINITY;
+      if (et <= e0 + 1e-12 * std::fabs(e0)) { have_trial_energy = true; break; }
+      gamma *= 0.5;
+      halvings += 1;
+    }
+    memcpy(&acts_ls, C.h_res + R_NSLOTS, sizeof(int));
+    if (info) info->line_search_activations = acts_ls + halvings;
+  } else if (info) {
+    info->line_search_activations = 0;
+  }
+  double e_trial = C.h_res[R_ENERGY];
+  C.phase_begin(6, C.nv * 96.0);
+  k_finalize<<<red_grid(C.nv), kBlock, 0, C.stream>>>(C.nv, C.x, C.dx, gamma, guard ? 1 : 0,
+                                                       C.partials + R_DX2 * kMaxPartials,
+                                                       C.counters + R_DX2, C.res);
+  C.check_launch();
+  C.phase_end();
+  if (C.track_energy && !have_trial_energy) launch_energy(C, nullptr, 0.0, R_ENERGY);
+  JGS2_CUDA(cudaMemcpyAsync(C.h_res, C.res, R_NSLOTS * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+  C.sync();
+  if (info) {
+    info->grad_sq = C.h_res[R_GRADSQ];
+    info->grad_norm = std::sqrt(C.h_res[R_GRADSQ]);
+    info->max_local_step = C.h_res[R_DXMAX];
+    info->dx_norm = C.norm_scale * std::sqrt(C.h_res[R_DX2]);
+    info->energy = have_trial_energy ? e_trial : C.h_res[R_ENERGY];
+    info->halvings = halvings;
+    info->n_pairs = pairs_at_start;
+  }
+}
+
+}  // namespace
+
+// ============================================================= lifecycle
+extern "C" {
+
+int32_t jgs2_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+jgs2_ctx* jgs2_create(int32_t device) {
+  int n = jgs2_device_count();
+  if (n <= 0 || device < 0 || device >= n) return nullptr;
+  jgs2_ctx* ctx = new jgs2_ctx();
+  ctx->c.device = device;
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return nullptr;
+  }
+  try {
+    Ctx& C = ctx->c;
+    C.partials = C.alloc<double>((size_t)R_NSLOTS * kMaxPartials);
+    C.counters = C.alloc<unsigned>(R_NSLOTS);
+    C.res = C.alloc<double>(R_NSLOTS);
+    JGS2_CUDA(cudaMemset(C.counters, 0, R_NSLOTS * sizeof(unsigned)));
+    JGS2_CUDA(cudaMemset(C.res, 0, R_NSLOTS * sizeof(double)));
+    JGS2_CUDA(cudaMallocHost(&C.h_res, 2 * R_NSLOTS * sizeof(double)));
+    cudaFuncSetAttribute(k_forward_level, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSmemCapDoubles * (int)sizeof(double));
+    cudaFuncSetAttribute(k_backward_level, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSmemCapDoubles * (int)sizeof(double));
+  } catch (...) {
+    delete ctx;
+    return nullptr;
+  }
+  return ctx;
+}
+
+void jgs2_destroy(jgs2_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->c.device);
+  delete ctx;
+}
+
+const char* jgs2_last_error(const jgs2_ctx* ctx) { return ctx ? ctx->c.err.c_str() : "null context"; }
+
+// ============================================================= setup
+int32_t jgs2_set_model(jgs2_ctx* ctx, const jgs2_model* md) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (!md || md->nv <= 0 || md->ne < 0) throw Error(JGS2_E_ARG, "invalid model sizes");
+    if (C.have_model) throw Error(JGS2_E_ARG, "model already set (create a new context)");
+    C.nv = (int)md->nv;
+    C.ne = (int)md->ne;
+    const int nv = C.nv, ne = C.ne;
+    C.norm_scale = md->norm_scale;
+    C.h_tets.assign(md->tets, md->tets + 4 * (size_t)ne);
+    std::vector<int4> t4(ne);
+    for (int e = 0; e < ne; ++e) {
+      for (int a = 0; a < 4; ++a) {
+        int64_t w = md->tets[4 * (size_t)e + a];
+        if (w < 0 || w >= nv) throw Error(JGS2_E_ARG, "element references a vertex out of range");
+      }
+      t4[e] = make_int4((int)md->tets[4 * (size_t)e], (int)md->tets[4 * (size_t)e + 1],
+                        (int)md->tets[4 * (size_t)e + 2], (int)md->tets[4 * (size_t)e + 3]);
+    }
+    C.tets = C.upload(t4.data(), ne);
+    C.dminv = C.upload(md->dm_inv, 9 * (size_t)ne);
+    std::vector<double4> ep(ne);
+    for (int e = 0; e < ne; ++e)
+      ep[e] = make_double4(md->volumes[e], md->mu[e], md->lam[e], md->elem_qmass[e]);
+    C.eprops = C.upload(ep.data(), ne);
+    // incidence CSR, ascending element id per vertex
+    std::vector<int> cnt(nv + 1, 0), inc(4 * (size_t)ne);
+    for (size_t k = 0; k < 4 * (size_t)ne; ++k) cnt[md->tets[k] + 1]++;
+    for (int v = 0; v < nv; ++v) cnt[v + 1] += cnt[v];
+    std::vector<int> fill(cnt.begin(), cnt.end() - 1);
+    for (int e = 0; e < ne; ++e)
+      for (int a = 0; a < 4; ++a) inc[fill[md->tets[4 * (size_t)e + a]]++] = 4 * e + a;
+    C.inc_ptr = C.upload(cnt.data(), nv + 1);
+    C.inc = C.upload(inc.data(), 4 * (size_t)ne);
+    C.mass = C.upload(md->masses, nv);
+    C.h_fixed.assign(md->fixed_mask, md->fixed_mask + nv);
+    C.fixed = C.upload(md->fixed_mask, nv);
+    C.h_rest.assign(md->rest_positions, md->rest_positions + 3 * (size_t)nv);
+    C.rest = C.upload(md->rest_positions, 3 * (size_t)nv);
+    std::vector<int> freel;
+    for (int v = 0; v < nv; ++v)
+      if (!md->fixed_mask[v]) freel.push_back(v);
+    C.nfree = (int)freel.size();
+    C.free_list = C.upload(freel.data(), freel.size());
+    C.x = C.alloc<double>(3 * (size_t)nv);
+    C.z = C.alloc<double>(3 * (size_t)nv);
+    C.R = C.alloc<double>(9 * (size_t)nv);
+    C.gasm = C.alloc<double>(3 * (size_t)nv);
+    C.b = C.alloc<double>(3 * (size_t)std::max(C.nfree, 1));
+    C.delta = C.alloc<double>(3 * (size_t)nv);
+    C.dx = C.alloc<double>(3 * (size_t)nv);
+    C.alpha0 = C.alloc<double>(nv);
+    C.kacc = C.alloc<int>(nv);
+    JGS2_CUDA(cudaMemsetAsync(C.delta, 0, 3 * (size_t)nv * sizeof(double), C.stream));
+    JGS2_CUDA(cudaMemsetAsync(C.dx, 0, 3 * (size_t)nv * sizeof(double), C.stream));
+    contact_setup(C, md);
+    C.have_model = true;
+    C.sync();
+  });
+}
+
+int32_t jgs2_set_precompute(jgs2_ctx* ctx, const jgs2_precompute* p, const jgs2_config* cfg) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (!C.have_model) throw Error(JGS2_E_ARG, "set the model first");
+    if (!p || !cfg) throw Error(JGS2_E_ARG, "null precompute/config");
+    if (C.have_pre) throw Error(JGS2_E_ARG, "precompute already set");
+    C.tol_dx = cfg->tol_dx;
+    C.max_outer = cfg->max_outer;
+    C.local_line_search = cfg->local_line_search != 0;
+    C.track_energy = cfg->track_energy != 0;
+    C.max_halvings = cfg->max_halvings;
+    C.alpha_floor = cfg->alpha_floor;
+    if (C.tol_dx <= 0 || C.max_outer < 1 || C.max_halvings < 0)
+      throw Error(JGS2_E_ARG, "invalid solver config");
+    const int nv = C.nv;
+    const int64_t nb = p->n_bases;
+    C.gmax = (int)std::max<int64_t>(p->gmax, 1);
+    std::vector<int> bidx(nv, -1);
+    for (int64_t k = 0; k < nb; ++k) {
+      int64_t v = p->vertices[k];
+      if (v < 0 || v >= nv) throw Error(JGS2_E_ARG, "basis vertex out of range");
+      bidx[v] = (int)k;
+    }
+    for (int v = 0; v < nv; ++v)
+      if (!C.h_fixed[v] && bidx[v] < 0)
+        throw Error(JGS2_E_KEY, "free vertex " + std::to_string(v) + " has no basis");
+    std::vector<double> gbar(9 * (size_t)nv, 0.0), grows(9 * (size_t)C.gmax * nv, 0.0);
+    std::vector<int> group((size_t)C.gmax * nv, -1);
+    int smax = 0;
+    for (int v = 0; v < nv; ++v) {
+      int k = bidx[v];
+      if (k < 0 || C.h_fixed[v]) continue;
+      smax = std::max<int>(smax, (int)(p->cub_ptr[k + 1] - p->cub_ptr[k]));
+      for (int i = 0; i < 9; ++i) gbar[9 * (size_t)v + i] = p->gbar[9 * k + i];
+      for (int g = 0; g < p->gmax; ++g) group[(size_t)C.gmax * v + g] = (int)p->group[p->gmax * k + g];
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3 * p->gmax; ++c)
+          grows[9 * (size_t)C.gmax * v + 3 * C.gmax * r + c] = p->gbar_rows[(3 * p->gmax) * (3 * k + r) + c];
+    }
+    C.smax = smax;
+    C.gbar = C.upload(gbar.data(), gbar.size());
+    C.group = C.upload(group.data(), group.size());
+    C.grows = C.upload(grows.data(), grows.size());
+    // cubature slots
+    size_t ns = (size_t)nv * std::max(smax, 1);
+    std::vector<int> cub_e(ns, -1);
+    std::vector<double> cub_w(ns, 0.0), cub_rows(36 * ns, 0.0);
+    std::vector<int4> cub_verts(ns, make_int4(0, 0, 0, 0));
+    for (int v = 0; v < nv; ++v) {
+      int k = bidx[v];
+      if (k < 0 || C.h_fixed[v]) continue;
+      const int64_t* keys = p->vrows_keys + p->vrows_ptr[k];
+      int64_t nk = p->vrows_ptr[k + 1] - p->vrows_ptr[k];
+      for (int64_t s = p->cub_ptr[k]; s < p->cub_ptr[k + 1]; ++s) {
+        int slot = (int)(s - p->cub_ptr[k]);
+        int64_t e = p->cub_elems[s];
+        if (e < 0 || e >= C.ne) throw Error(JGS2_E_ARG, "cubature element out of range");
+        size_t vs = (size_t)v * smax + slot;
+        cub_e[vs] = (int)e;
+        cub_w[vs] = p->cub_weights[s];
+        int cs[4];
+        for (int a = 0; a < 4; ++a) {
+          int64_t w = C.h_tets[4 * e + a];
+          cs[a] = (int)w;
+          const int64_t* it = std::lower_bound(keys, keys + nk, w);
+          if (it == keys + nk || *it != w)
+            throw Error(JGS2_E_KEY, "basis at vertex " + std::to_string(v) + " lacks rows for vertex " +
+                                        std::to_string(w) + " of cubature element " + std::to_string(e));
+          const double* blk = p->vrows + 9 * (p->vrows_ptr[k] + (it - keys));
+          for (int i = 0; i < 9; ++i) cub_rows[36 * vs + 9 * a + i] = blk[i];
+        }
+        cub_verts[vs] = make_int4(cs[0], cs[1], cs[2], cs[3]);
+      }
+    }
+    std::vector<int> uniq;
+    for (int e : cub_e)
+      if (e >= 0) uniq.push_back(e);
+    std::sort(uniq.begin(), uniq.end());
+    uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+    C.nuniq = (int)uniq.size();
+    std::vector<int> cub_u(ns, -1);
+    for (size_t i = 0; i < ns; ++i)
+      if (cub_e[i] >= 0) cub_u[i] = (int)(std::lower_bound(uniq.begin(), uniq.end(), cub_e[i]) - uniq.begin());
+    C.cub_u = C.upload(cub_u.data(), ns);
+    C.cub_w = C.upload(cub_w.data(), ns);
+    C.cub_rows = C.upload(cub_rows.data(), 36 * ns);
+    C.cub_verts = C.upload(cub_verts.data(), ns);
+    C.uniq = C.upload(uniq.data(), uniq.size());
+    C.nslots = 0;
+    for (int e : cub_e) C.nslots += (e >= 0);
+    C.mplus = C.alloc<double>(45 * (size_t)std::max(C.nuniq, 1));
+    C.crest = C.alloc<double>(9 * (size_t)nv);
+    JGS2_CUDA(cudaMemsetAsync(C.crest, 0, 9 * (size_t)nv * sizeof(double), C.stream));
+    C.ls_max = C.alloc<unsigned long long>(C.max_halvings + 2);
+    C.ls_cnt = C.alloc<int>(C.max_halvings + 2);
+    C.ls_final = C.alloc<int>(4);
+    JGS2_CUDA(cudaMemsetAsync(C.ls_final, 0, 4 * sizeof(int), C.stream));
+    // retained rows CSR (contact coupling rows)
+    std::vector<int> vptr(nv + 1, 0), vkeys;
+    std::vector<double> vrows;
+    for (int v = 0; v < nv; ++v) {
+      int k = bidx[v];
+      if (k >= 0) {
+        for (int64_t q = p->vrows_ptr[k]; q < p->vrows_ptr[k + 1]; ++q) {
+          vkeys.push_back((int)p->vrows_keys[q]);
+          vrows.insert(vrows.end(), p->vrows + 9 * q, p->vrows + 9 * q + 9);
+        }
+      }
+      vptr[v + 1] = (int)vkeys.size();
+    }
+    if (contact_active(C)) {
+      C.vr_ptr = C.upload(vptr.data(), vptr.size());
+      C.vr_keys = C.upload(vkeys.data(), vkeys.size());
+      C.vr_rows = C.upload(vrows.data(), vrows.size());
+    }
+    // rest constant C_v with identity rotations and rest element Hessians
+    if (C.nuniq > 0) {
+      DevModel m = devmodel(C);
+      // pos is needed by devmodel consumers only after factoring; not used here
+      k_element_mplus<<<grid_for(C.nuniq, 128), 128, 0, C.stream>>>(C.nuniq, C.uniq, C.rest, C.tets,
+                                                                     C.dminv, C.eprops, C.mplus);
+      C.check_launch();
+      double* Rid = nullptr;
+      JGS2_CUDA(cudaMallocAsync(&Rid, 9 * (size_t)nv * sizeof(double), C.stream));
+      k_fill_identity<<<grid_for(nv), kBlock, 0, C.stream>>>(nv, Rid);
+      C.check_launch();
+      LocalArgs a = localargs(C);
+      a.R = Rid;
+      k_rest_constant<<<grid_for(C.nfree, 128), 128, 0, C.stream>>>(m, a, C.crest);
+      C.check_launch();
+      JGS2_CUDA(cudaFreeAsync(Rid, C.stream));
+    }
+    C.have_pre = true;
+    C.sync();
+  });
+}
+
+int32_t jgs2_factor_rest(jgs2_ctx* ctx, double h_ref, int32_t leaf_size, jgs2_factor_info* info) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (!C.have_model) throw Error(JGS2_E_ARG, "set the model first");
+    if (!(h_ref > 0)) throw Error(JGS2_E_ARG, "h_ref must be positive");
+    if (C.fac.ready) throw Error(JGS2_E_ARG, "factor already built");
+    factor_build(C, h_ref, leaf_size > 0 ? leaf_size : 32);
+    if (info) {
+      info->n_free = C.fac.nfree;
+      info->nnz_dof = C.fac.sym.nnz_dof;
+      info->nfronts = C.fac.nfronts;
+      info->nlevels = C.fac.nlevels;
+      info->max_front = C.fac.max_nf;
+      info->factor_seconds = C.fac.seconds;
+    }
+  });
+}
+
+int32_t jgs2_factor_blocks(jgs2_ctx* ctx, int64_t nblocks, const int64_t* brow, const int64_t* bcol,
+                           const double* bval, int32_t leaf_size, jgs2_factor_info* info) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (!C.have_model) throw Error(JGS2_E_ARG, "set the model first");
+    if (C.fac.ready) throw Error(JGS2_E_ARG, "factor already built");
+    BlockInput in{nblocks, brow, bcol, bval};
+    factor_build(C, 1.0, leaf_size > 0 ? leaf_size : 32, &in);
+    if (info) {
+      info->n_free = C.fac.nfree;
+      info->nnz_dof = C.fac.sym.nnz_dof;
+      info->nfronts = C.fac.nfronts;
+      info->nlevels = C.fac.nlevels;
+      info->max_front = C.fac.max_nf;
+      info->factor_seconds = C.fac.seconds;
+    }
+  });
+}
+
+// ============================================================= state
+int32_t jgs2_set_state(jgs2_ctx* ctx, const double* x, const double* z, double h) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (!C.have_model) throw Error(JGS2_E_ARG, "model not set");
+    if (!(h > 0)) throw Error(JGS2_E_ARG, "h must be positive");
+    size_t n = 3 * (size_t)C.nv * sizeof(double);
+    if (x) JGS2_CUDA(cudaMemcpyAsync(C.x, x, n, cudaMemcpyHostToDevice, C.stream));
+    if (z) JGS2_CUDA(cudaMemcpyAsync(C.z, z, n, cudaMemcpyHostToDevice, C.stream));
+    C.h = h;
+    C.sync();
+  });
+}
+
+int32_t jgs2_set_x(jgs2_ctx* ctx, const double* x) {
+  return guarded(ctx, [&](Ctx& C) {
+    JGS2_CUDA(cudaMemcpyAsync(C.x, x, 3 * (size_t)C.nv * sizeof(double), cudaMemcpyHostToDevice, C.stream));
+    C.sync();
+  });
+}
+
+int32_t jgs2_get_x(jgs2_ctx* ctx, double* x) {
+  return guarded(ctx, [&](Ctx& C) {
+    JGS2_CUDA(cudaMemcpyAsync(x, C.x, 3 * (size_t)C.nv * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    C.sync();
+  });
+}
+
+int32_t jgs2_get_dx(jgs2_ctx* ctx, double* dx) {
+  return guarded(ctx, [&](Ctx& C) {
+    JGS2_CUDA(cudaMemcpyAsync(dx, C.dx, 3 * (size_t)C.nv * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    C.sync();
+  });
+}
+
+int32_t jgs2_set_rotations(jgs2_ctx* ctx, const double* R) {
+  return guarded(ctx, [&](Ctx& C) {
+    JGS2_CUDA(cudaMemcpyAsync(C.R, R, 9 * (size_t)C.nv * sizeof(double), cudaMemcpyHostToDevice, C.stream));
+    C.rot_valid = true;
+    C.sync();
+  });
+}
+
+int32_t jgs2_get_rotations(jgs2_ctx* ctx, double* R) {
+  return guarded(ctx, [&](Ctx& C) {
+    JGS2_CUDA(cudaMemcpyAsync(R, C.R, 9 * (size_t)C.nv * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    C.sync();
+  });
+}
+
+// ============================================================= hot path
+int32_t jgs2_rotations(jgs2_ctx* ctx) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (!C.have_model) throw Error(JGS2_E_ARG, "model not set");
+    vertex_pass(C, true);
+    C.sync();
+  });
+}
+
+int32_t jgs2_sweep(jgs2_ctx* ctx, int32_t refresh_rotations, jgs2_sweep_info* info) {
+  return guarded(ctx, [&](Ctx& C) { sweep_core(C, refresh_rotations != 0, info); });
+}
+
+int32_t jgs2_sweep_host(jgs2_ctx* ctx, const double* x, const double* z, double h,
+                        const double* rotations, double* x_out, double* dx_out,
+                        jgs2_sweep_info* info) {
+  return guarded(ctx, [&](Ctx& C) {
+    size_t n = 3 * (size_t)C.nv * sizeof(double);
+    if (!(h > 0)) throw Error(JGS2_E_ARG, "h must be positive");
+    JGS2_CUDA(cudaMemcpyAsync(C.x, x, n, cudaMemcpyHostToDevice, C.stream));
+    JGS2_CUDA(cudaMemcpyAsync(C.z, z, n, cudaMemcpyHostToDevice, C.stream));
+    C.h = h;
+    if (rotations) {
+      JGS2_CUDA(cudaMemcpyAsync(C.R, rotations, 3 * n, cudaMemcpyHostToDevice, C.stream));
+      C.rot_valid = true;
+    }
+    sweep_core(C, rotations == nullptr, info);
+    if (x_out) JGS2_CUDA(cudaMemcpyAsync(x_out, C.x, n, cudaMemcpyDeviceToHost, C.stream));
+    if (dx_out) JGS2_CUDA(cudaMemcpyAsync(dx_out, C.dx, n, cudaMemcpyDeviceToHost, C.stream));
+    C.sync();
+  });
+}
+
+int32_t jgs2_outer_solve(jgs2_ctx* ctx, double* dx_norms, double* grad_norms, double* energies,
+                         double* max_local_steps, int64_t* activations, int32_t* iterations,
+                         int32_t* converged) {
+  return guarded(ctx, [&](Ctx& C) {
+    int it = 0;
+    bool conv = false;
+    for (; it < C.max_outer;) {
+      jgs2_sweep_info inf;
+      sweep_core(C, true, &inf);
+      if (dx_norms) dx_norms[it] = inf.dx_norm;
+      if (grad_norms) grad_norms[it] = inf.grad_norm;
+      if (energies) energies[it] = inf.energy;
+      if (max_local_steps) max_local_steps[it] = inf.max_local_step;
+      if (activations) activations[it] = inf.line_search_activations;
+      ++it;
+      if (inf.dx_norm < C.tol_dx) { conv = true; break; }
+    }
+    if (iterations) *iterations = it;
+    if (converged) *converged = conv ? 1 : 0;
+  });
+}
+
+// ============================================================= per-kernel entries
+int32_t jgs2_total_energy(jgs2_ctx* ctx, const double* x, double* energy) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (x) JGS2_CUDA(cudaMemcpyAsync(C.x, x, 3 * (size_t)C.nv * sizeof(double), cudaMemcpyHostToDevice, C.stream));
+    if (contact_active(C)) contact_find_pairs(C, C.x, nullptr, 0.0);
+    launch_energy(C, nullptr, 0.0, R_ENERGY);
+    JGS2_CUDA(cudaMemcpyAsync(C.h_res, C.res, R_NSLOTS * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    C.sync();
+    if (contact_active(C) && contact_infeasible(C)) throw Error(JGS2_E_INFEASIBLE, "barrier distance <= 0");
+    *energy = C.h_res[R_ENERGY];
+  });
+}
+
+int32_t jgs2_assembled_field(jgs2_ctx* ctx, double* g) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (contact_active(C)) contact_find_pairs(C, C.x, nullptr, 0.0);
+    vertex_pass(C, false);
+    if (contact_active(C)) contact_add_gradients(C);
+    JGS2_CUDA(cudaMemcpyAsync(g, C.gasm, 3 * (size_t)C.nv * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    C.sync();
+  });
+}
+
+int32_t jgs2_reduced_collect(jgs2_ctx* ctx, const double* R, const double* g, double* q) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (!C.fac.ready) throw Error(JGS2_E_ARG, "rest factor not built");
+    size_t n = 3 * (size_t)C.nv * sizeof(double);
+    JGS2_CUDA(cudaMemcpyAsync(C.R, R, 3 * n, cudaMemcpyHostToDevice, C.stream));
+    JGS2_CUDA(cudaMemcpyAsync(C.gasm, g, n, cudaMemcpyHostToDevice, C.stream));
+    C.rot_valid = true;
+    collect(C);
+    std::vector<double> b(3 * (size_t)std::max(C.nfree, 1)), out(3 * (size_t)C.nv, 0.0);
+    std::vector<int> pos(C.nv);
+    JGS2_CUDA(cudaMemcpyAsync(b.data(), C.b, 3 * (size_t)C.nfree * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    JGS2_CUDA(cudaMemcpyAsync(pos.data(), C.pos, C.nv * sizeof(int), cudaMemcpyDeviceToHost, C.stream));
+    C.sync();
+    for (int v = 0; v < C.nv; ++v)
+      if (pos[v] >= 0)
+        for (int c = 0; c < 3; ++c) out[3 * (size_t)v + c] = b[3 * (size_t)pos[v] + c];
+    memcpy(q, out.data(), n);
+  });
+}
+
+static void debug_systems(Ctx& C, double* a, double* g, double* corr) {
+  require_ready(C);
+  if (!C.rot_valid) throw Error(JGS2_E_ARG, "rotations not set");
+  if (contact_active(C)) contact_find_pairs(C, C.x, nullptr, 0.0);
+  vertex_pass(C, false);
+  if (contact_active(C)) contact_add_gradients(C);
+  collect(C);
+  size_t n9 = 9 * (size_t)C.nv;
+  double *dA = nullptr, *dg = nullptr, *dc = nullptr;
+  JGS2_CUDA(cudaMallocAsync(&dA, n9 * sizeof(double), C.stream));
+  JGS2_CUDA(cudaMallocAsync(&dg, n9 * sizeof(double), C.stream));
+  JGS2_CUDA(cudaMallocAsync(&dc, n9 * sizeof(double), C.stream));
+  JGS2_CUDA(cudaMemsetAsync(dA, 0, n9 * sizeof(double), C.stream));
+  JGS2_CUDA(cudaMemsetAsync(dg, 0, n9 * sizeof(double), C.stream));
+  JGS2_CUDA(cudaMemsetAsync(dc, 0, n9 * sizeof(double), C.stream));
+  local_systems(C, dA, dg, dc);
+  if (a) JGS2_CUDA(cudaMemcpyAsync(a, dA, n9 * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+  if (g) JGS2_CUDA(cudaMemcpyAsync(g, dg, 3 * (size_t)C.nv * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+  if (corr) JGS2_CUDA(cudaMemcpyAsync(corr, dc, n9 * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+  JGS2_CUDA(cudaFreeAsync(dA, C.stream));
+  JGS2_CUDA(cudaFreeAsync(dg, C.stream));
+  JGS2_CUDA(cudaFreeAsync(dc, C.stream));
+  C.sync();
+}
+
+int32_t jgs2_sampled_corrections(jgs2_ctx* ctx, double* corr) {
+  return guarded(ctx, [&](Ctx& C) { debug_systems(C, nullptr, nullptr, corr); });
+}
+
+int32_t jgs2_reduced_systems(jgs2_ctx* ctx, double* a, double* g) {
+  return guarded(ctx, [&](Ctx& C) { debug_systems(C, a, g, nullptr); });
+}
+
+int32_t jgs2_find_pairs(jgs2_ctx* ctx, double* rows, int64_t capacity, int64_t* count) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (!contact_active(C)) { *count = 0; return; }
+    contact_find_pairs(C, C.x, nullptr, 0.0);
+    C.sync();
+    *count = C.npairs;
+    if (C.npairs > capacity) throw Error(JGS2_E_ARG, "pair capacity too small");
+    if (C.npairs)
+      JGS2_CUDA(cudaMemcpy(rows, C.pairs, (size_t)C.npairs * kPairRow * sizeof(double), cudaMemcpyDeviceToHost));
+  });
+}
+
+int32_t jgs2_last_kernel_launches(jgs2_ctx* ctx, int64_t* launches) {
+  if (!ctx || !launches) return JGS2_E_ARG;
+  *launches = ctx->c.launches;
+  return JGS2_OK;
+}
+
+// ============================================================= measurement
+int32_t jgs2_profile(jgs2_ctx* ctx, int32_t enable) {
+  return guarded(ctx, [&](Ctx& C) { C.sync(); C.profiling = enable != 0; });
+}
+
+int32_t jgs2_phase_stats(jgs2_ctx* ctx, double* ms, int64_t* launches, double* bytes) {
+  return guarded(ctx, [&](Ctx& C) {
+    C.sync();
+    for (int p = 0; p < Ctx::kPhases; ++p) {
+      if (ms) ms[p] = C.phase_ms[p];
+      if (launches) launches[p] = C.phase_launch[p];
+      if (bytes) bytes[p] = C.phase_bytes[p];
+    }
+  });
+}
+
+int32_t jgs2_phase_reset(jgs2_ctx* ctx) {
+  return guarded(ctx, [&](Ctx& C) {
+    C.sync();
+    for (int p = 0; p < Ctx::kPhases; ++p) { C.phase_ms[p] = 0; C.phase_launch[p] = 0; C.phase_bytes[p] = 0; }
+  });
+}
+
+int32_t jgs2_timer_start(jgs2_ctx* ctx) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (!C.tstart) { JGS2_CUDA(cudaEventCreate(&C.tstart)); JGS2_CUDA(cudaEventCreate(&C.tstop)); }
+    JGS2_CUDA(cudaEventRecord(C.tstart, C.stream));
+  });
+}
+
+int32_t jgs2_timer_stop(jgs2_ctx* ctx, double* ms) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (!C.tstart) throw Error(JGS2_E_ARG, "timer not started");
+    JGS2_CUDA(cudaEventRecord(C.tstop, C.stream));
+    JGS2_CUDA(cudaEventSynchronize(C.tstop));
+    float f = 0.f;
+    JGS2_CUDA(cudaEventElapsedTime(&f, C.tstart, C.tstop));
+    *ms = f;
+  });
+}
+
+void* jgs2_pinned_alloc(int64_t bytes) {
+  void* p = nullptr;
+  if (cudaMallocHost(&p, (size_t)std::max<int64_t>(bytes, 1)) != cudaSuccess) return nullptr;
+  return p;
+}
+
+void jgs2_pinned_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+int32_t jgs2_step_cap(jgs2_ctx* ctx, const double* x, const double* dx, double* cap) {
+  return guarded(ctx, [&](Ctx& C) {
+    *cap = 1.0;
+    if (!contact_active(C)) return;
+    size_t n = 3 * (size_t)C.nv * sizeof(double);
+    double *dxd = nullptr;
+    JGS2_CUDA(cudaMemcpyAsync(C.x, x, n, cudaMemcpyHostToDevice, C.stream));
+    JGS2_CUDA(cudaMallocAsync(&dxd, n, C.stream));
+    JGS2_CUDA(cudaMemcpyAsync(dxd, dx, n, cudaMemcpyHostToDevice, C.stream));
+    *cap = contact_step_cap(C, C.x, dxd);
+    JGS2_CUDA(cudaFreeAsync(dxd, C.stream));
+    C.sync();
+  });
+}
+
+// ============================================================= symbolic (host only)
+jgs2_sym* jgs2_sym_build(int64_t n, const int64_t* adj_ptr, const int32_t* adj, const double* coords,
+                         int32_t leaf_size) {
+  try {
+    jgs2_sym* s = new jgs2_sym();
+    build_symbolic((int)n, adj_ptr, adj, coords, leaf_size, s->s);
+    return s;
+  } catch (...) {
+    return nullptr;
+  }
+}
+
+int32_t jgs2_sym_sizes(const jgs2_sym* s, int64_t* sizes) {
+  if (!s || !sizes) return JGS2_E_ARG;
+  sizes[0] = s->s.nfronts;
+  sizes[1] = (int64_t)s->s.struct_pos.size();
+  sizes[2] = s->s.nlevels;
+  sizes[3] = s->s.nnz_dof;
+  return JGS2_OK;
+}
+
+int32_t jgs2_sym_export(const jgs2_sym* s, int32_t* perm, int32_t* parent, int32_t* col_begin,
+                        int32_t* col_end, int64_t* struct_ptr, int32_t* struct_pos, int32_t* level) {
+  if (!s) return JGS2_E_ARG;
+  const Symbolic& S = s->s;
+  if (perm) std::copy(S.perm.begin(), S.perm.end(), perm);
+  if (parent) std::copy(S.parent.begin(), S.parent.end(), parent);
+  if (col_begin) std::copy(S.col_begin.begin(), S.col_begin.end(), col_begin);
+  if (col_end) std::copy(S.col_end.begin(), S.col_end.end(), col_end);
+  if (struct_ptr) std::copy(S.struct_ptr.begin(), S.struct_ptr.end(), struct_ptr);
+  if (struct_pos) std::copy(S.struct_pos.begin(), S.struct_pos.end(), struct_pos);
+  if (level) std::copy(S.level.begin(), S.level.end(), level);
+  return JGS2_OK;
+}
+
+void jgs2_sym_free(jgs2_sym* s) { delete s; }
+
+}  // extern "C"

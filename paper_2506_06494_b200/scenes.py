@@ -1,0 +1,131 @@
+"""Synthetic benchmark scenes (BASELINE.json ``configs``).
+
+* ``c1``  cantilever ~10K tets, no contact (the reference's CPU scene):
+          box_grid((24,10,7),(1.2,0.5,0.35)), clamped at x=0, E=1e6.
+* ``c3``  stiff beam twist, ~1M tets, no contact: box_grid((160,40,26)),
+          clamped at x=0, E=2e7, initial angular velocity about the beam axis
+          ramped along x (the reference's acceptance "kick" ramp,
+          test_acceptance.py:139-145, turned into a twist).
+* ``c2`` / ``c4`` puffer balls (voxel SDF spheres with spikes -> Kuhn tets)
+          dropping onto a ground plane / into a five-plane glass tank with
+          IPC barrier contact (``cube_drop.toml`` barrier settings).
+
+All scenes use gravity (0, -9.8, 0), rho = 1000, nu = 0.4, h = 1/120 and
+seed 0; random-init precompute is ``Precompute.injected`` (structurally
+valid, see precompute.py) wherever the reference precompute cannot run.
+"""
+
+import numpy as np
+
+from .model import (BarrierParams, HalfSpace, MaterialParams, Model, SystemState, box_grid,
+                    build_mesh, compute_z)
+
+H = 1.0 / 120.0
+
+
+def cantilever(divisions=(24, 10, 7), extents=(1.2, 0.5, 0.35), young=1e6):
+    mesh = box_grid(divisions, extents)
+    mat = MaterialParams.from_young_poisson(young, 0.4, 1000.0)
+    fixed = np.flatnonzero(mesh.rest_positions[:, 0] < 1e-9)
+    return Model([(mesh, mat, fixed, np.zeros(3), np.eye(3))])
+
+
+def twist_state(model, h=H, omega=2.0):
+    """Initial state with an angular velocity about the beam's long axis,
+    ramped linearly from the clamped end (x = 0) to the free end."""
+    x0 = model.initial_positions
+    st = SystemState.initial(model, h)
+    w = x0[:, 0] / max(x0[:, 0].max(), 1e-300)
+    c = 0.5 * (x0.min(axis=0) + x0.max(axis=0))
+    ry, rz = x0[:, 1] - c[1], x0[:, 2] - c[2]
+    st.v[:, 1] = -omega * w * rz
+    st.v[:, 2] = omega * w * ry
+    st.v[model.fixed_mask] = 0.0
+    return st
+
+
+def puffer_ball_mesh(radius=0.5, cells=40, spikes=12, spike_amp=0.25, seed=0, center=(0, 0, 0)):
+    """Kuhn-tet voxelisation of a spiky sphere SDF (cells across the
+    diameter). Keeps voxels whose centre is inside the SDF."""
+    rng = np.random.default_rng(seed)
+    dirs = rng.standard_normal((spikes, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    ext = 2.0 * radius * (1.0 + spike_amp)
+    n = int(np.ceil(cells * (1.0 + spike_amp)))
+    dx = ext / n
+    g = (np.arange(n) + 0.5) * dx - ext / 2
+    X, Y, Zc = np.meshgrid(g, g, g, indexing="ij")
+    p = np.stack([X.ravel(), Y.ravel(), Zc.ravel()], axis=1)
+    r = np.linalg.norm(p, axis=1)
+    u = p / np.maximum(r, 1e-12)[:, None]
+    bump = np.max(np.clip(u @ dirs.T, 0.0, 1.0) ** 16, axis=1)
+    inside = r <= radius * (1.0 + spike_amp * bump)
+    cell = np.flatnonzero(inside.reshape(n, n, n).ravel())
+    i, j, k = np.unravel_index(cell, (n, n, n))
+    # Kuhn split on the shared vertex lattice
+    c = np.arange(8)
+    ci = i[:, None] + (c >> 2 & 1)
+    cj = j[:, None] + (c >> 1 & 1)
+    ck = k[:, None] + (c & 1)
+    vid = (ci * (n + 1) + cj) * (n + 1) + ck
+    from .model import _KUHN
+    tets = vid[:, _KUHN].reshape(-1, 4)
+    used, inv = np.unique(tets, return_inverse=True)
+    tets = inv.reshape(-1, 4)
+    li, lj, lk = np.unravel_index(used, (n + 1, n + 1, n + 1))
+    verts = np.stack([li, lj, lk], axis=1) * dx - ext / 2 + np.asarray(center, dtype=np.float64)
+    return build_mesh(verts, tets)
+
+
+def puffer_balls(n_balls=1, cells=40, young=2e7, soft_young=None, plane_only=True, gap=0.15):
+    """C2 (n_balls=1, ground plane) / C4 (10 balls, glass tank) scene."""
+    bodies = []
+    meshes = []
+    r = 0.5
+    for b in range(n_balls):
+        m = puffer_ball_mesh(radius=r, cells=cells, seed=b)
+        meshes.append(m)
+    ext = 2 * r * 1.25
+    per_row = max(1, int(np.ceil(np.sqrt(n_balls))))
+    for b, m in enumerate(meshes):
+        e = young if (soft_young is None or b % 2 == 0) else soft_young
+        mat = MaterialParams.from_young_poisson(e, 0.4, 1000.0)
+        ix, iz = b % per_row, (b // per_row) % per_row
+        iy = b // (per_row * per_row)
+        t = np.array([ix * (ext + gap), ext / 2 + 0.05 + iy * (ext + gap), iz * (ext + gap)])
+        bodies.append((m, mat, np.zeros(0, dtype=np.int64), t, np.eye(3)))
+    dhat = 0.01 * ext
+    planes = [HalfSpace(np.zeros(3), np.array([0.0, 1.0, 0.0]))]
+    if not plane_only:
+        lo = -ext / 2 - gap
+        hi = (per_row - 1) * (ext + gap) + ext / 2 + gap
+        planes += [HalfSpace(np.array([lo, 0, 0]), np.array([1.0, 0, 0])),
+                   HalfSpace(np.array([hi, 0, 0]), np.array([-1.0, 0, 0])),
+                   HalfSpace(np.array([0, 0, lo]), np.array([0, 0, 1.0])),
+                   HalfSpace(np.array([0, 0, hi]), np.array([0, 0, -1.0]))]
+    return Model(bodies, planes=planes, barrier=BarrierParams(dhat=dhat, kappa=2e3))
+
+
+def predictor_state(model, state):
+    """z from the state's velocity; x at the (unconstrained) predictor."""
+    compute_z(model, state)
+    state.x = state.z.copy()
+    return state
+
+
+def build(name):
+    """(model, state, h, description) for a named config."""
+    if name == "c1":
+        m = cantilever()
+        st = SystemState.initial(m, H)
+        return m, predictor_state(m, st), H, "C1 cantilever box_grid(24,10,7) 10,080 tets, E=1e6, no contact"
+    if name == "c3":
+        m = cantilever(divisions=(160, 40, 26), extents=(8.0, 2.0, 1.3), young=2e7)
+        return m, predictor_state(m, twist_state(m)), H, \
+            "C3 stiff beam twist box_grid(160,40,26) 998,400 tets, E=2e7, no contact"
+    if name.startswith("c3s"):  # scaled-down C3 for tests / CPU samples: c3s<k>
+        k = int(name[3:] or 4)
+        m = cantilever(divisions=(160 // k, 40 // k, max(26 // k, 2)),
+                       extents=(8.0, 2.0, 1.3), young=2e7)
+        return m, predictor_state(m, twist_state(m)), H, f"C3/{k} twist beam"
+    raise ValueError(f"unknown scene {name!r}")

@@ -221,6 +221,10 @@ def c1_scene():
     return scene, model
 
 
+# (frame, sweep) of the per-kernel snapshot: a deformed state, in contact
+# for the contact scenes.
+SNAPSHOT = {"cube_drop": (20, 2), "two_body": (25, 2)}
+
 SCENES = {
     "beam": lambda: scene_from_toml("beam"),
     "beam_stiff": lambda: scene_from_toml("beam_stiff", frames=3),
@@ -246,7 +250,8 @@ def main(names):
                                       cfg.alpha_floor, float(cfg.local_line_search),
                                       float(cfg.track_energy)])
         t1 = time.time()
-        data.update(run_trajectory(model, solver, scene.h, frames))
+        data.update(run_trajectory(model, solver, scene.h, frames,
+                                   record_kernels_at=SNAPSHOT.get(name, (2, 1))))
         t_run = time.time() - t1
         data["meta_versions"] = np.array([np.__version__, scipy.__version__])
         data["meta_times"] = np.array([t_pre, t_run])
