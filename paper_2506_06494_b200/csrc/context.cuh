@@ -65,6 +65,9 @@ struct Factor {
   int* level_fronts = nullptr; // fronts grouped by level
   std::vector<int> level_ptr;  // host
   std::vector<int> level_maxnf;
+  int4* fwd_tasks = nullptr;   // (front, row_begin, row_end)
+  int4* bwd_tasks = nullptr;   // (front, col_begin, col_end)
+  std::vector<int> fwd_level_ptr, bwd_level_ptr, fwd_level_smem, bwd_level_smem;
   double* u = nullptr;         // update vectors
   double* w = nullptr;         // work vectors (global fallback)
   int max_nf = 0;
@@ -124,7 +127,8 @@ struct Ctx {
   double* z = nullptr;
   double* R = nullptr;         // nv*9
   double* gasm = nullptr;      // nv*3
-  double* b = nullptr;         // 3*nfree (rhs / solution, ND order)
+  double* b = nullptr;         // 3*nfree (rhs, then forward result; ND order)
+  double* q = nullptr;         // 3*nfree collect solution q (ND order)
   double* delta = nullptr;     // nv*3
   double* alpha0 = nullptr;    // nv
   int* kacc = nullptr;         // nv accept iteration of the local search

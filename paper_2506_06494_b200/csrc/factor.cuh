@@ -115,20 +115,34 @@ __global__ void k_extend_add(int nrc, const double* Uc, const int* rmap, int nsp
 }
 
 // ------------------------------------------------------------------ solve kernels
+// Partitioned-inverse storage (Alvarado-Pothen style): every front keeps
+//   P = [ L11^-1 ; W ],  W = L21 L11^-1   (nf x ns, column major, ld nf)
+// so the forward step of a front is one matvec  t = P v_s
+//   z_s = t[0:ns],  u = v_r - t[ns:nf]
+// and the backward step one transposed matvec  x_s = P^T [z_s ; -x_r].
+// There is no dependency chain inside a front: a front's rows (forward) or
+// columns (backward) are split over many CTAs; fronts depend only on their
+// children (forward) / ancestors (backward), one launch per tree level.
 constexpr int kSolveThreads = 256;
-constexpr int kSmemCapDoubles = 24576;  // 192 KB
+constexpr int kSmemCapDoubles = 16384;  // 128 KB vector cache
 
-// Forward substitution L z = y for all fronts of one level (one CTA each).
+__global__ void k_zero_upper(int ns, int nf, double* P) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t tot = (int64_t)ns * ns;
+  if (idx >= tot) return;
+  int r = (int)(idx % ns), c = (int)(idx / ns);
+  if (r < c) P[(int64_t)c * nf + r] = 0.0;
+}
+
+// forward assembly: v_f = [y_cols ; 0] + extend-add of the children's
+// update vectors (children in ascending order: deterministic)
 __global__ void __launch_bounds__(kSolveThreads)
-k_forward_level(const int* fronts, const int* colbeg, const int* f_ns, const int* f_nr,
-                const int64_t* loff, const int64_t* uoff, const int64_t* woff, const int* cptr,
-                const int* clist, const int64_t* sptr, const int* rmap, const double* L,
-                double* b, double* u, double* wglob) {
-  extern __shared__ double smem[];
+k_fwd_assemble(const int* fronts, const int* colbeg, const int* f_ns, const int* f_nr,
+               const int64_t* uoff, const int64_t* woff, const int* cptr, const int* clist,
+               const int64_t* sptr, const int* rmap, const double* b, const double* u, double* w) {
   int f = fronts[blockIdx.x];
-  int ns = f_ns[f], nr = f_nr[f], nf = ns + nr;
-  double* v = (nf <= kSmemCapDoubles) ? smem : (wglob + woff[f]);
-  const double* P = L + loff[f];
+  int ns = f_ns[f], nf = ns + f_nr[f];
+  double* v = w + woff[f];
   int cb = colbeg[f];
   for (int i = threadIdx.x; i < nf; i += blockDim.x) v[i] = (i < ns) ? b[cb + i] : 0.0;
   __syncthreads();
@@ -140,85 +154,92 @@ k_forward_level(const int* fronts, const int* colbeg, const int* f_ns, const int
     for (int i = threadIdx.x; i < nrc; i += blockDim.x) v[rm[i]] += uc[i];
     __syncthreads();
   }
-  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int j0 = 0; j0 < ns; j0 += 32) {
-    int jb = min(32, ns - j0);
-    if (warp == 0) {
-      for (int jj = 0; jj < jb; ++jj) {
-        int j = j0 + jj;
-        double zj = v[j] / P[(int64_t)j * nf + j];
-        __syncwarp();
-        if (lane == jj) v[j] = zj;
-        if (lane > jj && lane < jb) v[j0 + lane] -= P[(int64_t)j * nf + j0 + lane] * zj;
-        __syncwarp();
-      }
-    }
-    __syncthreads();
-    for (int i = j0 + jb + threadIdx.x; i < nf; i += blockDim.x) {
-      double acc = 0.0;
-      for (int k = 0; k < jb; ++k) acc += P[(int64_t)(j0 + k) * nf + i] * v[j0 + k];
-      v[i] -= acc;
-    }
-    __syncthreads();
+}
+
+// forward apply, task = (front, row_begin, row_end): rows of t = P v_s
+__global__ void __launch_bounds__(kSolveThreads)
+k_fwd_apply(const int4* tasks, const int* colbeg, const int* f_ns, const int* f_nr,
+            const int64_t* loff, const int64_t* uoff, const int64_t* woff, const double* __restrict__ L,
+            const double* __restrict__ w, double* b, double* u) {
+  extern __shared__ double sv[];
+  __shared__ double red[8][33];
+  int4 tk = tasks[blockIdx.x];
+  int f = tk.x, r0 = tk.y, r1 = tk.z;
+  int ns = f_ns[f], nf = ns + f_nr[f];
+  const double* P = L + loff[f];
+  const double* v = w + woff[f];
+  int cmax = min(ns, r1);
+  const double* vs = v;
+  if (cmax <= kSmemCapDoubles) {
+    for (int i = threadIdx.x; i < cmax; i += blockDim.x) sv[i] = v[i];
+    vs = sv;
   }
-  for (int i = threadIdx.x; i < nf; i += blockDim.x) {
-    if (i < ns) b[cb + i] = v[i];
-    else u[uoff[f] + (i - ns)] = v[i];
+  __syncthreads();
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int cb = colbeg[f];
+  for (int i0 = r0; i0 < r1; i0 += 32) {
+    int row = i0 + lane;
+    int cend = min(ns, i0 + 32);
+    double acc0 = 0.0, acc1 = 0.0;
+    if (row < r1) {
+      const double* Pr = P + row;
+      int j = warp;
+      for (; j + 8 < cend; j += 16) {
+        acc0 += __ldg(Pr + (int64_t)j * nf) * vs[j];
+        acc1 += __ldg(Pr + (int64_t)(j + 8) * nf) * vs[j + 8];
+      }
+      if (j < cend) acc0 += __ldg(Pr + (int64_t)j * nf) * vs[j];
+    }
+    red[warp][lane] = acc0 + acc1;
+    __syncthreads();
+    if (warp == 0 && row < r1) {
+      double t = ((red[0][lane] + red[1][lane]) + (red[2][lane] + red[3][lane])) +
+                 ((red[4][lane] + red[5][lane]) + (red[6][lane] + red[7][lane]));
+      if (row < ns) b[cb + row] = t;
+      else u[uoff[f] + (row - ns)] = v[row] - t;
+    }
+    __syncthreads();
   }
 }
 
-// Backward substitution L^T x = z for all fronts of one level.
+// backward apply, task = (front, col_begin, col_end): x_j = P[:, j] . [z ; -x_r]
 __global__ void __launch_bounds__(kSolveThreads)
-k_backward_level(const int* fronts, const int* colbeg, const int* f_ns, const int* f_nr,
-                 const int64_t* loff, const int64_t* woff, const int64_t* sptr, const int* sdof,
-                 const double* L, double* b, double* wglob) {
-  extern __shared__ double smem[];
-  int f = fronts[blockIdx.x];
-  int ns = f_ns[f], nr = f_nr[f], nf = ns + nr;
-  if (ns == 0) return;
-  double* t = (nf <= kSmemCapDoubles) ? smem : (wglob + woff[f]);
-  double* xg = t + ns;
+k_bwd_apply(const int4* tasks, const int* colbeg, const int* f_ns, const int* f_nr,
+            const int64_t* loff, const int64_t* sptr, const int* sdof, const double* __restrict__ L,
+            const double* b, double* q) {
+  extern __shared__ double sw[];
+  int4 tk = tasks[blockIdx.x];
+  int f = tk.x, c0 = tk.y, c1 = tk.z;
+  int ns = f_ns[f], nf = ns + f_nr[f];
   const double* P = L + loff[f];
   int cb = colbeg[f];
   const int* sd = sdof + sptr[f];
-  for (int i = threadIdx.x; i < nf; i += blockDim.x) t[i] = (i < ns) ? b[cb + i] : b[sd[i - ns]];
+  int len = nf - c0;
+  bool cached = len <= kSmemCapDoubles;
+  if (cached) {
+    for (int i = threadIdx.x; i < len; i += blockDim.x) {
+      int r = c0 + i;
+      sw[i] = (r < ns) ? b[cb + r] : -q[sd[r - ns]];
+    }
+  }
   __syncthreads();
-  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  if (nr > 0) {
-    for (int j = warp; j < ns; j += nw) {
-      const double* col = P + (int64_t)j * nf + ns;
-      double acc = 0.0;
-      for (int k = lane; k < nr; k += 32) acc += col[k] * xg[k];
-      acc = warp_sum(acc);
-      if (lane == 0) t[j] -= acc;
-    }
-    __syncthreads();
-  }
-  for (int j1 = ns; j1 > 0; j1 -= 32) {
-    int j0 = max(0, j1 - 32);
-    if (j1 < ns) {
-      for (int j = j0 + warp; j < j1; j += nw) {
-        const double* col = P + (int64_t)j * nf;
-        double acc = 0.0;
-        for (int i = j1 + lane; i < ns; i += 32) acc += col[i] * t[i];
-        acc = warp_sum(acc);
-        if (lane == 0) t[j] -= acc;
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = c0 + warp; j < c1; j += 8) {
+    const double* col = P + (int64_t)j * nf;
+    double acc0 = 0.0, acc1 = 0.0;
+    int i = j + lane;
+    if (cached) {
+      for (; i + 32 < nf; i += 64) {
+        acc0 += __ldg(col + i) * sw[i - c0];
+        acc1 += __ldg(col + i + 32) * sw[i + 32 - c0];
       }
-      __syncthreads();
+      if (i < nf) acc0 += __ldg(col + i) * sw[i - c0];
+    } else {
+      for (; i < nf; i += 32) acc0 += __ldg(col + i) * ((i < ns) ? b[cb + i] : -q[sd[i - ns]]);
     }
-    if (warp == 0) {
-      for (int jj = j1 - 1; jj >= j0; --jj) {
-        double xj = t[jj] / P[(int64_t)jj * nf + jj];
-        __syncwarp();
-        int jr = j0 + lane;
-        if (jr < jj) t[jr] -= P[(int64_t)jr * nf + jj] * xj;
-        if (lane == 0) t[jj] = xj;
-        __syncwarp();
-      }
-    }
-    __syncthreads();
+    double acc = warp_sum(acc0 + acc1);
+    if (lane == 0) q[cb + j] = acc;
   }
-  for (int i = threadIdx.x; i < ns; i += blockDim.x) b[cb + i] = t[i];
 }
 
 // ------------------------------------------------------------------ host side
@@ -332,6 +353,62 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
   F.level_maxnf.assign(F.nlevels, 0);
   for (int f = 0; f < NF; ++f)
     F.level_maxnf[S.level[f]] = std::max(F.level_maxnf[S.level[f]], fns[f] + fnr[f]);
+  // ---- solve task lists: per level, split fronts into row blocks (forward,
+  // multiples of 32 rows) / column blocks (backward, multiples of 8
+  // columns) of roughly equal entry counts; enough tasks to fill 2 waves.
+  {
+    std::vector<int4> ft, bt;
+    F.fwd_level_ptr.assign(F.nlevels + 1, 0);
+    F.bwd_level_ptr.assign(F.nlevels + 1, 0);
+    F.fwd_level_smem.assign(F.nlevels, 0);
+    F.bwd_level_smem.assign(F.nlevels, 0);
+    for (int l = 0; l < F.nlevels; ++l) {
+      double work = 0;
+      for (int k = F.level_ptr[l]; k < F.level_ptr[l + 1]; ++k) {
+        int f = lf[k];
+        double ns = fns[f], nr = fnr[f];
+        work += ns * (ns + 1) / 2 + nr * ns + nr;
+      }
+      double T = std::max(work / (2.0 * 148), 8192.0);
+      for (int k = F.level_ptr[l]; k < F.level_ptr[l + 1]; ++k) {
+        int f = lf[k];
+        int ns = fns[f], nf = fns[f] + fnr[f];
+        // forward rows
+        int r0 = 0;
+        double acc = 0;
+        for (int i0 = 0; i0 < nf; i0 += 32) {
+          int rows = std::min(32, nf - i0);
+          int cols = std::min(ns, i0 + 32);
+          acc += (double)rows * std::max(cols, 1);
+          if (acc >= T || i0 + 32 >= nf) {
+            int r1 = std::min(nf, i0 + 32);
+            ft.push_back(make_int4(f, r0, r1, 0));
+            F.fwd_level_smem[l] = std::max(F.fwd_level_smem[l], std::min(ns, r1));
+            r0 = r1;
+            acc = 0;
+          }
+        }
+        // backward columns
+        int c0 = 0;
+        acc = 0;
+        for (int j = 0; j < ns; j += 8) {
+          int cols = std::min(8, ns - j);
+          acc += (double)cols * (nf - j);
+          if (acc >= T || j + 8 >= ns) {
+            int c1 = std::min(ns, j + 8);
+            bt.push_back(make_int4(f, c0, c1, 0));
+            F.bwd_level_smem[l] = std::max(F.bwd_level_smem[l], nf - c0);
+            c0 = c1;
+            acc = 0;
+          }
+        }
+      }
+      F.fwd_level_ptr[l + 1] = (int)ft.size();
+      F.bwd_level_ptr[l + 1] = (int)bt.size();
+    }
+    F.fwd_tasks = C.upload(ft.data(), ft.size());
+    F.bwd_tasks = C.upload(bt.data(), bt.size());
+  }
   // ---- device metadata
   F.f_colbeg = C.upload(colbeg.data(), NF);
   F.f_ns = C.upload(fns.data(), NF);
@@ -434,8 +511,17 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
                                   &lwork) != CUSOLVER_STATUS_SUCCESS)
     throw Error(-2, "potrf buffer size");
   double* work = C.alloc<double>(std::max(lwork, 1));
-  int* infos = C.alloc<int>(NF);
-  JGS2_CUDA(cudaMemsetAsync(infos, 0, NF * sizeof(int), C.stream));
+  int* infos = C.alloc<int>(2 * NF);
+  int* infos2 = infos + NF;
+  JGS2_CUDA(cudaMemsetAsync(infos, 0, 2 * NF * sizeof(int), C.stream));
+  size_t tri_dbytes = 0, tri_hbytes = 0;
+  if (max_ns > 0 &&
+      cusolverDnXtrtri_bufferSize(C.cusolver, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, max_ns,
+                                  CUDA_R_64F, F.L, max_ns + 1, &tri_dbytes, &tri_hbytes) !=
+          CUSOLVER_STATUS_SUCCESS)
+    throw Error(-2, "trtri buffer size");
+  void* tri_d = C.alloc<char>(std::max<size_t>(tri_dbytes, 16));
+  std::vector<char> tri_h(std::max<size_t>(tri_hbytes, 16));
   std::vector<double*> Ubuf(NF, nullptr);
   const double one = 1.0, mone = -1.0;
   for (int f = 0; f < NF; ++f) {
@@ -469,37 +555,58 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
                         &one, Ubuf[f], nr) != CUBLAS_STATUS_SUCCESS)
           throw Error(-2, "cublasDsyrk failed");
       }
+      // partitioned inverse: L11 -> L11^-1 (strict upper zeroed), L21 -> L21 L11^-1
+      if (cusolverDnXtrtri(C.cusolver, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, ns, CUDA_R_64F,
+                           Pf, nf, tri_d, tri_dbytes, tri_h.data(), tri_hbytes, infos2 + f) !=
+          CUSOLVER_STATUS_SUCCESS)
+        throw Error(-2, "cusolverDnXtrtri failed");
+      k_zero_upper<<<grid_for((int64_t)ns * ns), kBlock, 0, C.stream>>>(ns, nf, Pf);
+      C.check_launch();
+      if (nr > 0 &&
+          cublasDtrmm(C.cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N,
+                      CUBLAS_DIAG_NON_UNIT, nr, ns, &one, Pf, nf, Pf + ns, nf, Pf + ns, nf) !=
+              CUBLAS_STATUS_SUCCESS)
+        throw Error(-2, "cublasDtrmm failed");
     }
   }
   for (int f = 0; f < NF; ++f)
     if (Ubuf[f]) JGS2_CUDA(cudaFreeAsync(Ubuf[f], C.stream));
-  std::vector<int> hinfo(NF);
-  JGS2_CUDA(cudaMemcpyAsync(hinfo.data(), infos, NF * sizeof(int), cudaMemcpyDeviceToHost, C.stream));
+  std::vector<int> hinfo(2 * NF);
+  JGS2_CUDA(cudaMemcpyAsync(hinfo.data(), infos, 2 * NF * sizeof(int), cudaMemcpyDeviceToHost, C.stream));
   C.sync();
-  for (int f = 0; f < NF; ++f)
-    if (hinfo[f] != 0) throw Error(-3, "rest Hessian factorization failed: front " + std::to_string(f) +
-                                           " not positive definite (info " + std::to_string(hinfo[f]) + ")");
+  for (int f = 0; f < 2 * NF; ++f)
+    if (hinfo[f] != 0)
+      throw Error(-3, std::string("rest Hessian factorization failed: front ") + std::to_string(f % NF) +
+                          (f < NF ? " not positive definite" : " singular diagonal block") +
+                          " (info " + std::to_string(hinfo[f]) + ")");
   F.ready = true;
   F.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
-// b <- Hbar_ff^{-1} b (ND-ordered DOFs): forward then backward level sweeps.
+// q <- Hbar_ff^{-1} b (ND-ordered DOFs): forward level sweeps (assemble +
+// apply) leaves z in b; backward level sweeps write x into q.
 void factor_solve(Ctx& C) {
   Factor& F = C.fac;
   for (int l = 0; l < F.nlevels; ++l) {
     int cnt = F.level_ptr[l + 1] - F.level_ptr[l];
-    size_t sm = std::min(F.level_maxnf[l], kSmemCapDoubles) * sizeof(double);
-    k_forward_level<<<cnt, kSolveThreads, sm, C.stream>>>(
-        F.level_fronts + F.level_ptr[l], F.f_colbeg, F.f_ns, F.f_nr, F.f_loff, F.f_uoff, F.f_woff,
-        F.f_cptr, F.f_clist, F.f_sptr, F.f_rmap, F.L, C.b, F.u, F.w);
+    k_fwd_assemble<<<cnt, kSolveThreads, 0, C.stream>>>(
+        F.level_fronts + F.level_ptr[l], F.f_colbeg, F.f_ns, F.f_nr, F.f_uoff, F.f_woff, F.f_cptr,
+        F.f_clist, F.f_sptr, F.f_rmap, C.b, F.u, F.w);
+    C.check_launch();
+    int nt = F.fwd_level_ptr[l + 1] - F.fwd_level_ptr[l];
+    size_t sm = std::min(F.fwd_level_smem[l], kSmemCapDoubles) * sizeof(double);
+    k_fwd_apply<<<nt, kSolveThreads, sm, C.stream>>>(F.fwd_tasks + F.fwd_level_ptr[l], F.f_colbeg,
+                                                     F.f_ns, F.f_nr, F.f_loff, F.f_uoff, F.f_woff,
+                                                     F.L, F.w, C.b, F.u);
     C.check_launch();
   }
   for (int l = F.nlevels - 1; l >= 0; --l) {
-    int cnt = F.level_ptr[l + 1] - F.level_ptr[l];
-    size_t sm = std::min(F.level_maxnf[l], kSmemCapDoubles) * sizeof(double);
-    k_backward_level<<<cnt, kSolveThreads, sm, C.stream>>>(
-        F.level_fronts + F.level_ptr[l], F.f_colbeg, F.f_ns, F.f_nr, F.f_loff, F.f_woff, F.f_sptr,
-        F.f_sdof, F.L, C.b, F.w);
+    int nt = F.bwd_level_ptr[l + 1] - F.bwd_level_ptr[l];
+    if (nt == 0) continue;
+    size_t sm = std::min(F.bwd_level_smem[l], kSmemCapDoubles) * sizeof(double);
+    k_bwd_apply<<<nt, kSolveThreads, sm, C.stream>>>(F.bwd_tasks + F.bwd_level_ptr[l], F.f_colbeg,
+                                                     F.f_ns, F.f_nr, F.f_loff, F.f_sptr, F.f_sdof,
+                                                     F.L, C.b, C.q);
     C.check_launch();
   }
 }

@@ -64,7 +64,7 @@ DevModel devmodel(const Ctx& C) {
 LocalArgs localargs(Ctx& C) {
   LocalArgs a;
   memset(&a, 0, sizeof(a));
-  a.R = C.R; a.b = C.b; a.gbar = C.gbar; a.group = C.group; a.grows = C.grows;
+  a.R = C.R; a.b = C.q; a.gbar = C.gbar; a.group = C.group; a.grows = C.grows;
   a.cub_u = C.cub_u; a.cub_w = C.cub_w; a.cub_rows = C.cub_rows; a.cub_verts = C.cub_verts;
   a.crest = C.crest; a.mplus = C.mplus; a.h = C.h;
   a.delta = C.delta; a.alpha0 = C.alpha0; a.kacc = C.kacc;
@@ -272,9 +272,9 @@ jgs2_ctx* jgs2_create(int32_t device) {
     JGS2_CUDA(cudaMemset(C.counters, 0, R_NSLOTS * sizeof(unsigned)));
     JGS2_CUDA(cudaMemset(C.res, 0, R_NSLOTS * sizeof(double)));
     JGS2_CUDA(cudaMallocHost(&C.h_res, 2 * R_NSLOTS * sizeof(double)));
-    cudaFuncSetAttribute(k_forward_level, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_fwd_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kSmemCapDoubles * (int)sizeof(double));
-    cudaFuncSetAttribute(k_backward_level, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_bwd_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kSmemCapDoubles * (int)sizeof(double));
   } catch (...) {
     delete ctx;
@@ -340,6 +340,7 @@ int32_t jgs2_set_model(jgs2_ctx* ctx, const jgs2_model* md) {
     C.R = C.alloc<double>(9 * (size_t)nv);
     C.gasm = C.alloc<double>(3 * (size_t)nv);
     C.b = C.alloc<double>(3 * (size_t)std::max(C.nfree, 1));
+    C.q = C.alloc<double>(3 * (size_t)std::max(C.nfree, 1));
     C.delta = C.alloc<double>(3 * (size_t)nv);
     C.dx = C.alloc<double>(3 * (size_t)nv);
     C.alpha0 = C.alloc<double>(nv);
@@ -660,7 +661,7 @@ int32_t jgs2_reduced_collect(jgs2_ctx* ctx, const double* R, const double* g, do
     collect(C);
     std::vector<double> b(3 * (size_t)std::max(C.nfree, 1)), out(3 * (size_t)C.nv, 0.0);
     std::vector<int> pos(C.nv);
-    JGS2_CUDA(cudaMemcpyAsync(b.data(), C.b, 3 * (size_t)C.nfree * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    JGS2_CUDA(cudaMemcpyAsync(b.data(), C.q, 3 * (size_t)C.nfree * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
     JGS2_CUDA(cudaMemcpyAsync(pos.data(), C.pos, C.nv * sizeof(int), cudaMemcpyDeviceToHost, C.stream));
     C.sync();
     for (int v = 0; v < C.nv; ++v)
