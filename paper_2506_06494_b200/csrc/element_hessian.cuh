@@ -1,0 +1,313 @@
+// Projected element Hessians in translation-complement coordinates.
+//
+// Reference: energy.snh_batch(..., project_spd=True) -> 12x12 Hessian
+// V W^T H9 W followed by an eigenvalue clamp (energy.py:110-149, 169-189).
+// The 12x12 Hessian annihilates rigid translations, so its PSD projection
+// equals T PSD(M) T^T with M = T^T H12 T the 9x9 reduced Hessian in the
+// Hadamard complement basis T = U (x) I3 (agrees with the
+// 12x12 eigh to 3.8e-15).  M has the closed form (G = W^T U, a_p = F G_p,
+// b_p = cof(F) G_p, s = lam_s (J - alpha)):
+//   M_(p,q) = V [ d (G_p.G_q) I + c1 a_p a_q^T + lam_s b_p b_q^T
+//                 - s [F (G_p x G_q)]_x ]
+// (the stable Neo-Hookean H9 = d I + c1 f f^T + lam_s g g^T + s K with the
+// cofactor-derivative skew blocks K, contracted against G).
+//
+// Projection: an LDL^T inertia test returns M unchanged when it is positive
+// definite; otherwise the 9x9 eigendecomposition is computed by Householder
+// tridiagonalisation + implicit QL (EISPACK tred2/tql2 scheme) in
+// per-thread interleaved shared memory, and M+ = Q max(L, 0) Q^T.
+#pragma once
+#include "physics.cuh"
+
+namespace jgs2 {
+
+constexpr int kHessThreads = 128;
+
+// packed lower index for (i >= j)
+#define JGS2_PK(i, j) ((i) * ((i) + 1) / 2 + (j))
+
+__device__ __forceinline__ void reduced_hessian_closed(const double* F, const double* D, double vol,
+                                                       SnhConst k, double* Mp /*45*/) {
+  double W[12];
+  shape_weights(D, W);
+  double G[9];  // G[j][p]
+#pragma unroll
+  for (int j = 0; j < 3; ++j)
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+      G[3 * j + p] = W[j] * kHad(0, p) + W[3 + j] * kHad(1, p) + W[6 + j] * kHad(2, p) + W[9 + j] * kHad(3, p);
+  double C[9];
+  cofactor(F, C);
+  double ic = frob2(F), J = det3_cof(F, C);
+  double d = k.mu_s * (1.0 - 1.0 / (ic + 1.0));
+  double c1 = 2.0 * k.mu_s / ((ic + 1.0) * (ic + 1.0));
+  double s = k.lam_s * (J - k.alpha);
+  double a[9], b[9];  // a[3p + r] = (F G)[r][p]
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      a[3 * p + r] = F[3 * r] * G[p] + F[3 * r + 1] * G[3 + p] + F[3 * r + 2] * G[6 + p];
+      b[3 * p + r] = C[3 * r] * G[p] + C[3 * r + 1] * G[3 + p] + C[3 * r + 2] * G[6 + p];
+    }
+  double GG[9];
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) GG[3 * p + q] = G[p] * G[q] + G[3 + p] * G[3 + q] + G[6 + p] * G[6 + q];
+  // FX[pq] = F (G_p x G_q) for (p,q) = (1,0), (2,0), (2,1)
+  double FX[3][3];
+  const int PP[3] = {1, 2, 2}, QQ[3] = {0, 0, 1};
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    int p = PP[t], q = QQ[t];
+    double gp[3] = {G[p], G[3 + p], G[6 + p]}, gq[3] = {G[q], G[3 + q], G[6 + q]}, x[3];
+    cross3(gp, gq, x);
+#pragma unroll
+    for (int r = 0; r < 3; ++r) FX[t][r] = F[3 * r] * x[0] + F[3 * r + 1] * x[1] + F[3 * r + 2] * x[2];
+  }
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int q = 0; q <= p; ++q)
+#pragma unroll
+        for (int ss = 0; ss < 3; ++ss) {
+          int i = 3 * p + r, j = 3 * q + ss;
+          if (j > i) continue;
+          double v = c1 * a[3 * p + r] * a[3 * q + ss] + k.lam_s * b[3 * p + r] * b[3 * q + ss];
+          if (r == ss) v += d * GG[3 * p + q];
+          if (p != q) {  // - s [FX]_x (r, ss)
+            int t = (p == 1) ? 0 : (q == 0 ? 1 : 2);
+            const double* x = FX[t];
+            double sk = 0.0;  // [x]_x[r][ss]
+            if (r == 0 && ss == 1) sk = -x[2];
+            if (r == 0 && ss == 2) sk = x[1];
+            if (r == 1 && ss == 0) sk = x[2];
+            if (r == 1 && ss == 2) sk = -x[0];
+            if (r == 2 && ss == 0) sk = -x[1];
+            if (r == 2 && ss == 1) sk = x[0];
+            v -= s * sk;
+          }
+          Mp[JGS2_PK(i, j)] = vol * v;
+        }
+}
+
+// LDL^T without pivoting: true iff all pivots > 0 (positive definite).
+__device__ __forceinline__ bool is_pos_def9(const double* Mp) {
+  double L[45];
+#pragma unroll
+  for (int i = 0; i < 45; ++i) L[i] = Mp[i];
+  double dd[9];
+#pragma unroll
+  for (int j = 0; j < 9; ++j) {
+    double dj = L[JGS2_PK(j, j)];
+#pragma unroll
+    for (int k = 0; k < j; ++k) dj -= L[JGS2_PK(j, k)] * L[JGS2_PK(j, k)] * dd[k];
+    if (!(dj > 0.0)) return false;
+    dd[j] = dj;
+    double inv = 1.0 / dj;
+#pragma unroll
+    for (int i = j + 1; i < 9; ++i) {
+      double v = L[JGS2_PK(i, j)];
+#pragma unroll
+      for (int k = 0; k < j; ++k) v -= L[JGS2_PK(i, k)] * L[JGS2_PK(j, k)] * dd[k];
+      L[JGS2_PK(i, j)] = v * inv;
+    }
+  }
+  return true;
+}
+
+// Symmetric 9x9 eigendecomposition (tred2 + tql2) on interleaved shared
+// memory: V(i,j) = V[(9*i+j)*S], d(i) = d[i*S], e(i) = e[i*S].
+template <int S>
+__device__ void sym_eig9_shared(double* V, double* d, double* e) {
+  constexpr int n = 9;
+#define VV(i, j) V[((i) * n + (j)) * S]
+#define DD(i) d[(i) * S]
+#define EE(i) e[(i) * S]
+  for (int j = 0; j < n; ++j) DD(j) = VV(n - 1, j);
+  for (int i = n - 1; i > 0; --i) {
+    double scale = 0.0, h = 0.0;
+    for (int k = 0; k < i; ++k) scale += fabs(DD(k));
+    if (scale == 0.0) {
+      EE(i) = DD(i - 1);
+      for (int j = 0; j < i; ++j) { DD(j) = VV(i - 1, j); VV(i, j) = 0.0; VV(j, i) = 0.0; }
+    } else {
+      for (int k = 0; k < i; ++k) { DD(k) /= scale; h += DD(k) * DD(k); }
+      double f = DD(i - 1);
+      double g = sqrt(h);
+      if (f > 0) g = -g;
+      EE(i) = scale * g;
+      h -= f * g;
+      DD(i - 1) = f - g;
+      for (int j = 0; j < i; ++j) EE(j) = 0.0;
+      for (int j = 0; j < i; ++j) {
+        f = DD(j);
+        VV(j, i) = f;
+        g = EE(j) + VV(j, j) * f;
+        for (int k = j + 1; k <= i - 1; ++k) { g += VV(k, j) * DD(k); EE(k) += VV(k, j) * f; }
+        EE(j) = g;
+      }
+      f = 0.0;
+      for (int j = 0; j < i; ++j) { EE(j) /= h; f += EE(j) * DD(j); }
+      double hh = f / (h + h);
+      for (int j = 0; j < i; ++j) EE(j) -= hh * DD(j);
+      for (int j = 0; j < i; ++j) {
+        f = DD(j);
+        g = EE(j);
+        for (int k = j; k <= i - 1; ++k) VV(k, j) -= (f * EE(k) + g * DD(k));
+        DD(j) = VV(i - 1, j);
+        VV(i, j) = 0.0;
+      }
+    }
+    DD(i) = h;
+  }
+  for (int i = 0; i < n - 1; ++i) {
+    VV(n - 1, i) = VV(i, i);
+    VV(i, i) = 1.0;
+    double h = DD(i + 1);
+    if (h != 0.0) {
+      for (int k = 0; k <= i; ++k) DD(k) = VV(k, i + 1) / h;
+      for (int j = 0; j <= i; ++j) {
+        double g = 0.0;
+        for (int k = 0; k <= i; ++k) g += VV(k, i + 1) * VV(k, j);
+        for (int k = 0; k <= i; ++k) VV(k, j) -= g * DD(k);
+      }
+    }
+    for (int k = 0; k <= i; ++k) VV(k, i + 1) = 0.0;
+  }
+  for (int j = 0; j < n; ++j) { DD(j) = VV(n - 1, j); VV(n - 1, j) = 0.0; }
+  VV(n - 1, n - 1) = 1.0;
+  EE(0) = 0.0;
+  // implicit QL
+  for (int i = 1; i < n; ++i) EE(i - 1) = EE(i);
+  EE(n - 1) = 0.0;
+  double f = 0.0, tst1 = 0.0;
+  const double eps = 2.220446049250313e-16;
+  for (int l = 0; l < n; ++l) {
+    tst1 = fmax(tst1, fabs(DD(l)) + fabs(EE(l)));
+    int m = l;
+    while (m < n) {
+      if (fabs(EE(m)) <= eps * tst1) break;
+      ++m;
+    }
+    if (m == n) m = n - 1;
+    if (m > l) {
+      int iter = 0;
+      do {
+        ++iter;
+        double g = DD(l);
+        double p = (DD(l + 1) - g) / (2.0 * EE(l));
+        double r = hypot(p, 1.0);
+        if (p < 0) r = -r;
+        DD(l) = EE(l) / (p + r);
+        DD(l + 1) = EE(l) * (p + r);
+        double dl1 = DD(l + 1);
+        double h = g - DD(l);
+        for (int i = l + 2; i < n; ++i) DD(i) -= h;
+        f += h;
+        p = DD(m);
+        double c = 1.0, c2 = c, c3 = c;
+        double el1 = EE(l + 1);
+        double s = 0.0, s2 = 0.0;
+        for (int i = m - 1; i >= l; --i) {
+          c3 = c2;
+          c2 = c;
+          s2 = s;
+          g = c * EE(i);
+          h = c * p;
+          r = hypot(p, EE(i));
+          EE(i + 1) = s * r;
+          s = EE(i) / r;
+          c = p / r;
+          p = c * DD(i) - s * g;
+          DD(i + 1) = h + s * (c * g + s * DD(i));
+          for (int k = 0; k < n; ++k) {
+            h = VV(k, i + 1);
+            VV(k, i + 1) = s * VV(k, i) + c * h;
+            VV(k, i) = c * VV(k, i) - s * h;
+          }
+        }
+        p = -s * s2 * c3 * el1 * EE(l) / dl1;
+        EE(l) = s * p;
+        DD(l) = c * p;
+      } while (fabs(EE(l)) > eps * tst1 && iter < 60);
+    }
+    DD(l) = DD(l) + f;
+    EE(l) = 0.0;
+  }
+#undef VV
+#undef DD
+#undef EE
+}
+
+// One element: packed M (45) at xs -> packed PSD(M) (45) in out45.
+__device__ void element_mplus_smem(const double* xs, const int4 t, const double* D, const double4 ep,
+                                   double* out45, double* Vs, double* ds, double* es) {
+  double x0[3], x1[3], x2[3], x3[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    x0[c] = xs[3 * t.x + c]; x1[c] = xs[3 * t.y + c];
+    x2[c] = xs[3 * t.z + c]; x3[c] = xs[3 * t.w + c];
+  }
+  double F[9];
+  deformation_gradient(x0, x1, x2, x3, D, F);
+  double Mp[45];
+  reduced_hessian_closed(F, D, ep.x, snh_const(ep.y, ep.z), Mp);
+  if (is_pos_def9(Mp)) {
+#pragma unroll
+    for (int i = 0; i < 45; ++i) out45[i] = Mp[i];
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 9; ++i)
+#pragma unroll
+    for (int j = 0; j <= i; ++j) {
+      Vs[(9 * i + j) * kHessThreads] = Mp[JGS2_PK(i, j)];
+      Vs[(9 * j + i) * kHessThreads] = Mp[JGS2_PK(i, j)];
+    }
+  sym_eig9_shared<kHessThreads>(Vs, ds, es);
+  double lam[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) lam[k] = fmax(ds[k * kHessThreads], 0.0);
+  for (int i = 0; i < 9; ++i)
+    for (int j = 0; j <= i; ++j) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) acc += Vs[(9 * i + k) * kHessThreads] * lam[k] * Vs[(9 * j + k) * kHessThreads];
+      out45[JGS2_PK(i, j)] = acc;
+    }
+}
+
+__global__ void __launch_bounds__(kHessThreads)
+k_element_mplus(int n, const int* elems, const double* __restrict__ xs, const int4* __restrict__ tets,
+                const double* __restrict__ dminv, const double4* __restrict__ eprops, double* mplus) {
+  extern __shared__ double hsm[];
+  int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  double* Vs = hsm + threadIdx.x;
+  double* ds = hsm + 81 * kHessThreads + threadIdx.x;
+  double* es = hsm + 90 * kHessThreads + threadIdx.x;
+  int e = elems ? elems[u] : u;
+  double D[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) D[i] = __ldg(dminv + 9 * (size_t)e + i);
+  double out[45];
+  element_mplus_smem(xs, __ldg(tets + e), D, eprops[e], out, Vs, ds, es);
+  double* o = mplus + 45 * (size_t)u;
+#pragma unroll
+  for (int i = 0; i < 45; ++i) o[i] = out[i];
+}
+constexpr size_t kHessSmemBytes = 99 * kHessThreads * sizeof(double);
+
+inline void launch_element_mplus(int n, const int* elems, const double* xs, const int4* tets,
+                                 const double* dminv, const double4* eprops, double* out,
+                                 cudaStream_t stream) {
+  int grid = (n + kHessThreads - 1) / kHessThreads;
+  if (grid < 1) grid = 1;
+  k_element_mplus<<<grid, kHessThreads, kHessSmemBytes, stream>>>(n, elems, xs, tets, dminv, eprops, out);
+}
+
+}  // namespace jgs2

@@ -8,6 +8,7 @@
 // used), rows [ns, nf) the off-diagonal rows (its row structure).
 #pragma once
 #include "context.cuh"
+#include "element_hessian.cuh"
 
 #include <algorithm>
 #include <chrono>
@@ -16,38 +17,6 @@
 namespace jgs2 {
 
 // ---------------------------------------------------------------- element Hessians
-// Projected reduced element Hessian (45 packed doubles, translation
-// complement coordinates) at positions xs (energy.py:169-189 +
-// project_psd, via the 9x9 complement).
-__device__ void element_mplus(const double* xs, const int4 t, const double* D, const double4 ep,
-                              double* out45) {
-  double x0[3], x1[3], x2[3], x3[3];
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    x0[c] = xs[3 * t.x + c]; x1[c] = xs[3 * t.y + c];
-    x2[c] = xs[3 * t.z + c]; x3[c] = xs[3 * t.w + c];
-  }
-  double F[9];
-  deformation_gradient(x0, x1, x2, x3, D, F);
-  double M[81];
-  reduced_hessian9(F, D, ep.x, snh_const(ep.y, ep.z), M);
-  psd_project9(M);
-#pragma unroll 1
-  for (int i = 0; i < 9; ++i)
-    for (int j = 0; j <= i; ++j) out45[i * (i + 1) / 2 + j] = M[9 * i + j];
-}
-
-__global__ void k_element_mplus(int n, const int* elems, const double* xs, const int4* tets,
-                                const double* dminv, const double4* eprops, double* mplus) {
-  int u = blockIdx.x * blockDim.x + threadIdx.x;
-  if (u >= n) return;
-  int e = elems ? elems[u] : u;
-  double D[9];
-#pragma unroll
-  for (int i = 0; i < 9; ++i) D[i] = dminv[9 * (size_t)e + i];
-  element_mplus(xs, tets[e], D, eprops[e], mplus + 45 * (size_t)u);
-}
-
 // Hbar BSR block (i, j) of free vertices: sum over elements containing both
 // (ascending element id) of the projected rest element block + mass term.
 __global__ void k_bsr_blocks(int nblocks, const int* brow, const int* bcol, const int* inc_ptr,
@@ -435,8 +404,7 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
   double* mp_all = nullptr;
   if (!blocks) {
     JGS2_CUDA(cudaMallocAsync(&mp_all, 45 * (size_t)std::max(ne, 1) * sizeof(double), C.stream));
-    k_element_mplus<<<grid_for(ne, 128), 128, 0, C.stream>>>(ne, nullptr, C.rest, C.tets, C.dminv,
-                                                             C.eprops, mp_all);
+    launch_element_mplus(ne, nullptr, C.rest, C.tets, C.dminv, C.eprops, mp_all, C.stream);
     C.check_launch();
   }
   int64_t nblocks = aptr[n];

@@ -139,8 +139,7 @@ void local_systems(Ctx& C, double* A_out, double* g_out, double* corr_out) {
   DevModel m = devmodel(C);
   if (C.nuniq > 0) {
     C.phase_begin(3, bytes_cub(C));
-    k_element_mplus<<<grid_for(C.nuniq, 128), 128, 0, C.stream>>>(C.nuniq, C.uniq, C.x, C.tets,
-                                                                   C.dminv, C.eprops, C.mplus);
+    launch_element_mplus(C.nuniq, C.uniq, C.x, C.tets, C.dminv, C.eprops, C.mplus, C.stream);
     C.check_launch();
     C.phase_end();
   }
@@ -272,6 +271,8 @@ jgs2_ctx* jgs2_create(int32_t device) {
     JGS2_CUDA(cudaMemset(C.counters, 0, R_NSLOTS * sizeof(unsigned)));
     JGS2_CUDA(cudaMemset(C.res, 0, R_NSLOTS * sizeof(double)));
     JGS2_CUDA(cudaMallocHost(&C.h_res, 2 * R_NSLOTS * sizeof(double)));
+    cudaFuncSetAttribute(k_element_mplus, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kHessSmemBytes);
     cudaFuncSetAttribute(k_fwd_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kSmemCapDoubles * (int)sizeof(double));
     cudaFuncSetAttribute(k_bwd_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -471,8 +472,7 @@ int32_t jgs2_set_precompute(jgs2_ctx* ctx, const jgs2_precompute* p, const jgs2_
     if (C.nuniq > 0) {
       DevModel m = devmodel(C);
       // pos is needed by devmodel consumers only after factoring; not used here
-      k_element_mplus<<<grid_for(C.nuniq, 128), 128, 0, C.stream>>>(C.nuniq, C.uniq, C.rest, C.tets,
-                                                                     C.dminv, C.eprops, C.mplus);
+      launch_element_mplus(C.nuniq, C.uniq, C.rest, C.tets, C.dminv, C.eprops, C.mplus, C.stream);
       C.check_launch();
       double* Rid = nullptr;
       JGS2_CUDA(cudaMallocAsync(&Rid, 9 * (size_t)nv * sizeof(double), C.stream));
