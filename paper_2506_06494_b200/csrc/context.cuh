@@ -68,6 +68,15 @@ struct Factor {
   int4* fwd_tasks = nullptr;   // (front, row_begin, row_end)
   int4* bwd_tasks = nullptr;   // (front, col_begin, col_end)
   std::vector<int> fwd_level_ptr, bwd_level_ptr, fwd_level_smem, bwd_level_smem;
+  std::vector<int64_t> asm_level_ptr, gat_level_ptr;
+  int64_t* asm_dst = nullptr;  // flat forward assembly map
+  int* asm_b = nullptr;
+  int64_t* asm_cp = nullptr;
+  int64_t* asm_src = nullptr;
+  int64_t* gat_dst = nullptr;  // flat backward gather map
+  int* gat_src = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  int64_t graph_launches = 0;
   double* u = nullptr;         // update vectors
   double* w = nullptr;         // work vectors (global fallback)
   int max_nf = 0;

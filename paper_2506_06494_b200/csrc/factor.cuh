@@ -125,12 +125,17 @@ k_fwd_assemble(const int* fronts, const int* colbeg, const int* f_ns, const int*
   }
 }
 
-// forward apply, task = (front, row_begin, row_end): rows of t = P v_s
+// forward apply, task = (front, row_begin, row_end): rows of t = P v_s.
+// Warps split the columns (w, w+8, ...), lanes the 32 rows of a chunk; 8
+// independent 256-B loads in flight per warp; partial sums reduced across
+// warps in a fixed order (deterministic).
+constexpr int kVecCache = 4096;  // doubles of the vector cached in smem (32 KB)
+
 __global__ void __launch_bounds__(kSolveThreads)
 k_fwd_apply(const int4* tasks, const int* colbeg, const int* f_ns, const int* f_nr,
             const int64_t* loff, const int64_t* uoff, const int64_t* woff, const double* __restrict__ L,
             const double* __restrict__ w, double* b, double* u) {
-  extern __shared__ double sv[];
+  __shared__ double sv[kVecCache];
   __shared__ double red[8][33];
   int4 tk = tasks[blockIdx.x];
   int f = tk.x, r0 = tk.y, r1 = tk.z;
@@ -139,7 +144,7 @@ k_fwd_apply(const int4* tasks, const int* colbeg, const int* f_ns, const int* f_
   const double* v = w + woff[f];
   int cmax = min(ns, r1);
   const double* vs = v;
-  if (cmax <= kSmemCapDoubles) {
+  if (cmax <= kVecCache) {
     for (int i = threadIdx.x; i < cmax; i += blockDim.x) sv[i] = v[i];
     vs = sv;
   }
@@ -149,17 +154,25 @@ k_fwd_apply(const int4* tasks, const int* colbeg, const int* f_ns, const int* f_
   for (int i0 = r0; i0 < r1; i0 += 32) {
     int row = i0 + lane;
     int cend = min(ns, i0 + 32);
-    double acc0 = 0.0, acc1 = 0.0;
+    double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0, a6 = 0, a7 = 0;
     if (row < r1) {
       const double* Pr = P + row;
+      const int64_t s8 = 8 * (int64_t)nf;
       int j = warp;
-      for (; j + 8 < cend; j += 16) {
-        acc0 += __ldg(Pr + (int64_t)j * nf) * vs[j];
-        acc1 += __ldg(Pr + (int64_t)(j + 8) * nf) * vs[j + 8];
+      for (; j + 56 < cend; j += 64) {
+        const double* p = Pr + (int64_t)j * nf;
+        a0 += __ldg(p) * vs[j];
+        a1 += __ldg(p + s8) * vs[j + 8];
+        a2 += __ldg(p + 2 * s8) * vs[j + 16];
+        a3 += __ldg(p + 3 * s8) * vs[j + 24];
+        a4 += __ldg(p + 4 * s8) * vs[j + 32];
+        a5 += __ldg(p + 5 * s8) * vs[j + 40];
+        a6 += __ldg(p + 6 * s8) * vs[j + 48];
+        a7 += __ldg(p + 7 * s8) * vs[j + 56];
       }
-      if (j < cend) acc0 += __ldg(Pr + (int64_t)j * nf) * vs[j];
+      for (; j < cend; j += 8) a0 += __ldg(Pr + (int64_t)j * nf) * vs[j];
     }
-    red[warp][lane] = acc0 + acc1;
+    red[warp][lane] = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
     __syncthreads();
     if (warp == 0 && row < r1) {
       double t = ((red[0][lane] + red[1][lane]) + (red[2][lane] + red[3][lane])) +
@@ -171,42 +184,78 @@ k_fwd_apply(const int4* tasks, const int* colbeg, const int* f_ns, const int* f_
   }
 }
 
-// backward apply, task = (front, col_begin, col_end): x_j = P[:, j] . [z ; -x_r]
+// flat forward assembly: w[dst] = b[bsrc] (or 0) + sum of the children's
+// update entries mapped to this position (child order, deterministic)
+__global__ void k_fwd_assemble_flat(int64_t n, const int64_t* dst, const int* bsrc, const int64_t* cp,
+                                    const int64_t* src, const double* b, const double* u, double* w) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  int bs = bsrc[k];
+  double acc = bs >= 0 ? b[bs] : 0.0;
+  for (int64_t q = cp[k]; q < cp[k + 1]; ++q) acc += u[src[q]];
+  w[dst[k]] = acc;
+}
+
+// flat backward gather: w[dst] = z (src >= 0, from b) or -x (src < 0, from q)
+__global__ void k_bwd_gather_flat(int64_t n, const int64_t* dst, const int* src, const double* b,
+                                  const double* q, double* w) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  int s = src[k];
+  w[dst[k]] = s >= 0 ? b[s] : -q[-1 - s];
+}
+
+// backward gather: w_f = [z_s ; -x_r] (contiguous, per front of the level)
+__global__ void __launch_bounds__(kSolveThreads)
+k_bwd_gather(const int* fronts, const int* colbeg, const int* f_ns, const int* f_nr,
+             const int64_t* woff, const int64_t* sptr, const int* sdof, const double* b,
+             const double* q, double* w) {
+  int f = fronts[blockIdx.x];
+  int ns = f_ns[f], nf = ns + f_nr[f];
+  if (ns == 0) return;
+  double* wf = w + woff[f];
+  int cb = colbeg[f];
+  const int* sd = sdof + sptr[f];
+  for (int i = threadIdx.x; i < nf; i += blockDim.x) wf[i] = (i < ns) ? b[cb + i] : -q[sd[i - ns]];
+}
+
+// backward apply, task = (front, col_begin, col_end): x_j = P[:, j] . w_f
 __global__ void __launch_bounds__(kSolveThreads)
 k_bwd_apply(const int4* tasks, const int* colbeg, const int* f_ns, const int* f_nr,
-            const int64_t* loff, const int64_t* sptr, const int* sdof, const double* __restrict__ L,
-            const double* b, double* q) {
-  extern __shared__ double sw[];
+            const int64_t* loff, const int64_t* woff, const double* __restrict__ L,
+            const double* __restrict__ w, double* q) {
+  __shared__ double sw[kVecCache];
   int4 tk = tasks[blockIdx.x];
   int f = tk.x, c0 = tk.y, c1 = tk.z;
   int ns = f_ns[f], nf = ns + f_nr[f];
   const double* P = L + loff[f];
-  int cb = colbeg[f];
-  const int* sd = sdof + sptr[f];
+  const double* wf = w + woff[f];
   int len = nf - c0;
-  bool cached = len <= kSmemCapDoubles;
-  if (cached) {
-    for (int i = threadIdx.x; i < len; i += blockDim.x) {
-      int r = c0 + i;
-      sw[i] = (r < ns) ? b[cb + r] : -q[sd[r - ns]];
-    }
+  const double* ws = wf + c0;
+  if (len <= kVecCache) {
+    for (int i = threadIdx.x; i < len; i += blockDim.x) sw[i] = wf[c0 + i];
+    ws = sw;
   }
   __syncthreads();
+  ws -= c0;  // index by absolute row
   int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int cb = colbeg[f];
   for (int j = c0 + warp; j < c1; j += 8) {
     const double* col = P + (int64_t)j * nf;
-    double acc0 = 0.0, acc1 = 0.0;
+    double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0, a6 = 0, a7 = 0;
     int i = j + lane;
-    if (cached) {
-      for (; i + 32 < nf; i += 64) {
-        acc0 += __ldg(col + i) * sw[i - c0];
-        acc1 += __ldg(col + i + 32) * sw[i + 32 - c0];
-      }
-      if (i < nf) acc0 += __ldg(col + i) * sw[i - c0];
-    } else {
-      for (; i < nf; i += 32) acc0 += __ldg(col + i) * ((i < ns) ? b[cb + i] : -q[sd[i - ns]]);
+    for (; i + 224 < nf; i += 256) {
+      a0 += __ldg(col + i) * ws[i];
+      a1 += __ldg(col + i + 32) * ws[i + 32];
+      a2 += __ldg(col + i + 64) * ws[i + 64];
+      a3 += __ldg(col + i + 96) * ws[i + 96];
+      a4 += __ldg(col + i + 128) * ws[i + 128];
+      a5 += __ldg(col + i + 160) * ws[i + 160];
+      a6 += __ldg(col + i + 192) * ws[i + 192];
+      a7 += __ldg(col + i + 224) * ws[i + 224];
     }
-    double acc = warp_sum(acc0 + acc1);
+    for (; i < nf; i += 32) a0 += __ldg(col + i) * ws[i];
+    double acc = warp_sum(((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7)));
     if (lane == 0) q[cb + j] = acc;
   }
 }
@@ -338,7 +387,7 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
         double ns = fns[f], nr = fnr[f];
         work += ns * (ns + 1) / 2 + nr * ns + nr;
       }
-      double T = std::max(work / (2.0 * 148), 8192.0);
+      double T = std::max(work / (8.0 * 148), 4096.0);
       for (int k = F.level_ptr[l]; k < F.level_ptr[l + 1]; ++k) {
         int f = lf[k];
         int ns = fns[f], nf = fns[f] + fnr[f];
@@ -376,6 +425,49 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
       F.bwd_level_ptr[l + 1] = (int)bt.size();
     }
     F.fwd_tasks = C.upload(ft.data(), ft.size());
+    // flat per-level assemble map (forward) and gather map (backward):
+    // one entry per front position; contributions in child order.
+    std::vector<int64_t> adst, acp(1, 0), asrc, gdst;
+    std::vector<int> ab, gsrc;
+    F.asm_level_ptr.assign(F.nlevels + 1, 0);
+    F.gat_level_ptr.assign(F.nlevels + 1, 0);
+    for (int l = 0; l < F.nlevels; ++l) {
+      for (int k = F.level_ptr[l]; k < F.level_ptr[l + 1]; ++k) {
+        int f = lf[k];
+        int ns = fns[f], nf = fns[f] + fnr[f];
+        std::vector<int> cnt(nf + 1, 0);
+        for (int q = cptr[f]; q < cptr[f + 1]; ++q) {
+          int c = clist[q];
+          for (int64_t t = sptr[c]; t < sptr[c + 1]; ++t) cnt[rmap[t] + 1]++;
+        }
+        for (int i = 0; i < nf; ++i) cnt[i + 1] += cnt[i];
+        std::vector<int64_t> src(cnt[nf]);
+        std::vector<int> fill(cnt.begin(), cnt.end() - 1);
+        for (int q = cptr[f]; q < cptr[f + 1]; ++q) {
+          int c = clist[q];
+          for (int64_t t = sptr[c]; t < sptr[c + 1]; ++t)
+            src[fill[rmap[t]]++] = uoff[c] + (t - sptr[c]);
+        }
+        for (int i = 0; i < nf; ++i) {
+          adst.push_back(woff[f] + i);
+          ab.push_back(i < ns ? colbeg[f] + i : -1);
+          for (int c = cnt[i]; c < cnt[i + 1]; ++c) asrc.push_back(src[c]);
+          acp.push_back((int64_t)asrc.size());
+          if (ns > 0) {
+            gdst.push_back(woff[f] + i);
+            gsrc.push_back(i < ns ? colbeg[f] + i : -1 - sdof[sptr[f] + (i - ns)]);
+          }
+        }
+      }
+      F.asm_level_ptr[l + 1] = (int64_t)adst.size();
+      F.gat_level_ptr[l + 1] = (int64_t)gdst.size();
+    }
+    F.asm_dst = C.upload(adst.data(), adst.size());
+    F.asm_b = C.upload(ab.data(), ab.size());
+    F.asm_cp = C.upload(acp.data(), acp.size());
+    F.asm_src = C.upload(asrc.data(), asrc.size());
+    F.gat_dst = C.upload(gdst.data(), gdst.size());
+    F.gat_src = C.upload(gsrc.data(), gsrc.size());
     F.bwd_tasks = C.upload(bt.data(), bt.size());
   }
   // ---- device metadata
@@ -552,31 +644,52 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
 }
 
 // q <- Hbar_ff^{-1} b (ND-ordered DOFs): forward level sweeps (assemble +
-// apply) leaves z in b; backward level sweeps write x into q.
-void factor_solve(Ctx& C) {
+// apply) leave z in b; backward level sweeps (gather + apply) write x into q.
+void factor_solve_launches(Ctx& C) {
   Factor& F = C.fac;
   for (int l = 0; l < F.nlevels; ++l) {
-    int cnt = F.level_ptr[l + 1] - F.level_ptr[l];
-    k_fwd_assemble<<<cnt, kSolveThreads, 0, C.stream>>>(
-        F.level_fronts + F.level_ptr[l], F.f_colbeg, F.f_ns, F.f_nr, F.f_uoff, F.f_woff, F.f_cptr,
-        F.f_clist, F.f_sptr, F.f_rmap, C.b, F.u, F.w);
+    int64_t na = F.asm_level_ptr[l + 1] - F.asm_level_ptr[l];
+    int64_t o = F.asm_level_ptr[l];
+    k_fwd_assemble_flat<<<grid_for(na), kBlock, 0, C.stream>>>(na, F.asm_dst + o, F.asm_b + o,
+                                                               F.asm_cp + o, F.asm_src, C.b, F.u, F.w);
     C.check_launch();
     int nt = F.fwd_level_ptr[l + 1] - F.fwd_level_ptr[l];
-    size_t sm = std::min(F.fwd_level_smem[l], kSmemCapDoubles) * sizeof(double);
-    k_fwd_apply<<<nt, kSolveThreads, sm, C.stream>>>(F.fwd_tasks + F.fwd_level_ptr[l], F.f_colbeg,
-                                                     F.f_ns, F.f_nr, F.f_loff, F.f_uoff, F.f_woff,
-                                                     F.L, F.w, C.b, F.u);
+    k_fwd_apply<<<nt, kSolveThreads, 0, C.stream>>>(F.fwd_tasks + F.fwd_level_ptr[l], F.f_colbeg,
+                                                    F.f_ns, F.f_nr, F.f_loff, F.f_uoff, F.f_woff,
+                                                    F.L, F.w, C.b, F.u);
     C.check_launch();
   }
   for (int l = F.nlevels - 1; l >= 0; --l) {
     int nt = F.bwd_level_ptr[l + 1] - F.bwd_level_ptr[l];
     if (nt == 0) continue;
-    size_t sm = std::min(F.bwd_level_smem[l], kSmemCapDoubles) * sizeof(double);
-    k_bwd_apply<<<nt, kSolveThreads, sm, C.stream>>>(F.bwd_tasks + F.bwd_level_ptr[l], F.f_colbeg,
-                                                     F.f_ns, F.f_nr, F.f_loff, F.f_sptr, F.f_sdof,
-                                                     F.L, C.b, C.q);
+    int64_t ng = F.gat_level_ptr[l + 1] - F.gat_level_ptr[l];
+    int64_t o = F.gat_level_ptr[l];
+    k_bwd_gather_flat<<<grid_for(ng), kBlock, 0, C.stream>>>(ng, F.gat_dst + o, F.gat_src + o, C.b,
+                                                             C.q, F.w);
+    C.check_launch();
+    k_bwd_apply<<<nt, kSolveThreads, 0, C.stream>>>(F.bwd_tasks + F.bwd_level_ptr[l], F.f_colbeg,
+                                                    F.f_ns, F.f_nr, F.f_loff, F.f_woff, F.L, F.w, C.q);
     C.check_launch();
   }
+}
+
+// The solve is replayed from a CUDA graph captured once (all pointers are
+// fixed for the life of the factor): ~4 launches per tree level.
+void factor_solve(Ctx& C) {
+  Factor& F = C.fac;
+  if (!F.graph_exec) {
+    int64_t l0 = C.launches;
+    JGS2_CUDA(cudaStreamBeginCapture(C.stream, cudaStreamCaptureModeThreadLocal));
+    factor_solve_launches(C);
+    cudaGraph_t g;
+    JGS2_CUDA(cudaStreamEndCapture(C.stream, &g));
+    JGS2_CUDA(cudaGraphInstantiate(&F.graph_exec, g, 0));
+    JGS2_CUDA(cudaGraphDestroy(g));
+    F.graph_launches = C.launches - l0;
+    C.launches = l0;
+  }
+  JGS2_CUDA(cudaGraphLaunch(F.graph_exec, C.stream));
+  C.launches += F.graph_launches;
 }
 
 }  // namespace jgs2

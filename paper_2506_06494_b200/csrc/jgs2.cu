@@ -24,6 +24,7 @@ jgs2::Ctx::~Ctx() {
   if (tstop) cudaEventDestroy(tstop);
   if (cublas) cublasDestroy(cublas);
   if (cusolver) cusolverDnDestroy(cusolver);
+  if (fac.graph_exec) cudaGraphExecDestroy(fac.graph_exec);
   if (stream) cudaStreamDestroy(stream);
 }
 
@@ -273,10 +274,7 @@ jgs2_ctx* jgs2_create(int32_t device) {
     JGS2_CUDA(cudaMallocHost(&C.h_res, 2 * R_NSLOTS * sizeof(double)));
     cudaFuncSetAttribute(k_element_mplus, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kHessSmemBytes);
-    cudaFuncSetAttribute(k_fwd_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kSmemCapDoubles * (int)sizeof(double));
-    cudaFuncSetAttribute(k_bwd_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kSmemCapDoubles * (int)sizeof(double));
+
   } catch (...) {
     delete ctx;
     return nullptr;
