@@ -155,6 +155,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     world, rank, local, dist = dist_setup()
+    from paper_2506_06494_b200 import build as _build
+    _build.build()  # no-op unless a CUDA source is newer than lib/libjgs2.so
     metric = "JGS2 iterations/sec (sweeps/s) and ms per timestep to residual tol"
 
     from paper_2506_06494_b200 import scenes

@@ -54,6 +54,7 @@ struct Factor {
   int* f_colbeg = nullptr;     // first DOF position
   int* f_ns = nullptr;         // columns (DOF)
   int* f_nr = nullptr;         // struct rows (DOF)
+  int* f_ld = nullptr;         // panel leading dimension (nf rounded up to even)
   int64_t* f_loff = nullptr;   // panel offset in L (ld = ns + nr)
   int64_t* f_uoff = nullptr;   // update-vector offset (nr entries)
   int64_t* f_woff = nullptr;   // work-vector offset (nf entries)

@@ -126,61 +126,75 @@ k_fwd_assemble(const int* fronts, const int* colbeg, const int* f_ns, const int*
 }
 
 // forward apply, task = (front, row_begin, row_end): rows of t = P v_s.
-// Warps split the columns (w, w+8, ...), lanes the 32 rows of a chunk; 8
-// independent 256-B loads in flight per warp; partial sums reduced across
-// warps in a fixed order (deterministic).
+// Persistent CTAs stride over the level's tasks. Lanes own row pairs
+// (double2 loads: 512 B per warp-load, columns are 16-B aligned since ld is
+// even), warps split the columns (w, w+8, ...), 8 loads in flight per warp;
+// partial sums are combined across warps in a fixed order (deterministic).
 constexpr int kVecCache = 4096;  // doubles of the vector cached in smem (32 KB)
+constexpr int kApplyCtasPerSm = 4;
 
-__global__ void __launch_bounds__(kSolveThreads)
-k_fwd_apply(const int4* tasks, const int* colbeg, const int* f_ns, const int* f_nr,
-            const int64_t* loff, const int64_t* uoff, const int64_t* woff, const double* __restrict__ L,
-            const double* __restrict__ w, double* b, double* u) {
+__global__ void __launch_bounds__(kSolveThreads, kApplyCtasPerSm)
+k_fwd_apply(const int4* tasks, int ntasks, const int* colbeg, const int* f_ns, const int* f_nr,
+            const int* f_ld, const int64_t* loff, const int64_t* uoff, const int64_t* woff,
+            const double* __restrict__ L, const double* __restrict__ w, double* b, double* u) {
   __shared__ double sv[kVecCache];
-  __shared__ double red[8][33];
-  int4 tk = tasks[blockIdx.x];
-  int f = tk.x, r0 = tk.y, r1 = tk.z;
-  int ns = f_ns[f], nf = ns + f_nr[f];
-  const double* P = L + loff[f];
-  const double* v = w + woff[f];
-  int cmax = min(ns, r1);
-  const double* vs = v;
-  if (cmax <= kVecCache) {
-    for (int i = threadIdx.x; i < cmax; i += blockDim.x) sv[i] = v[i];
-    vs = sv;
-  }
-  __syncthreads();
+  __shared__ double red[8][65];
   int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int cb = colbeg[f];
-  for (int i0 = r0; i0 < r1; i0 += 32) {
-    int row = i0 + lane;
-    int cend = min(ns, i0 + 32);
-    double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0, a6 = 0, a7 = 0;
-    if (row < r1) {
-      const double* Pr = P + row;
-      const int64_t s8 = 8 * (int64_t)nf;
-      int j = warp;
-      for (; j + 56 < cend; j += 64) {
-        const double* p = Pr + (int64_t)j * nf;
-        a0 += __ldg(p) * vs[j];
-        a1 += __ldg(p + s8) * vs[j + 8];
-        a2 += __ldg(p + 2 * s8) * vs[j + 16];
-        a3 += __ldg(p + 3 * s8) * vs[j + 24];
-        a4 += __ldg(p + 4 * s8) * vs[j + 32];
-        a5 += __ldg(p + 5 * s8) * vs[j + 40];
-        a6 += __ldg(p + 6 * s8) * vs[j + 48];
-        a7 += __ldg(p + 7 * s8) * vs[j + 56];
+  for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
+    int4 tk = tasks[t];
+    int f = tk.x, r0 = tk.y, r1 = tk.z;
+    int ns = f_ns[f], nf = ns + f_nr[f], ld = f_ld[f];
+    const double* P = L + loff[f];
+    const double* v = w + woff[f];
+    int cmax = min(ns, r1);
+    const double* vs = v;
+    __syncthreads();  // previous task done with sv
+    if (cmax <= kVecCache) {
+      for (int i = threadIdx.x; i < cmax; i += blockDim.x) sv[i] = v[i];
+      vs = sv;
+    }
+    __syncthreads();
+    int cb = colbeg[f];
+    for (int i0 = r0; i0 < r1; i0 += 64) {
+      int row = i0 + 2 * lane;  // rows row, row + 1 (row + 1 may be the zero pad row)
+      int cend = min(ns, i0 + 64);
+      double a0 = 0, a1 = 0, a2 = 0, a3 = 0, b0 = 0, b1 = 0, b2 = 0, b3 = 0;
+      if (row < r1) {
+        const double2* Pr = reinterpret_cast<const double2*>(P + row);
+        const int64_t s = (int64_t)ld / 2;  // column stride in double2
+        int j = warp;
+        for (; j + 24 < cend; j += 32) {
+          double2 p0 = __ldg(Pr + (int64_t)j * s);
+          double2 p1 = __ldg(Pr + (int64_t)(j + 8) * s);
+          double2 p2 = __ldg(Pr + (int64_t)(j + 16) * s);
+          double2 p3 = __ldg(Pr + (int64_t)(j + 24) * s);
+          double v0 = vs[j], v1 = vs[j + 8], v2 = vs[j + 16], v3 = vs[j + 24];
+          a0 += p0.x * v0; b0 += p0.y * v0;
+          a1 += p1.x * v1; b1 += p1.y * v1;
+          a2 += p2.x * v2; b2 += p2.y * v2;
+          a3 += p3.x * v3; b3 += p3.y * v3;
+        }
+        for (; j < cend; j += 8) {
+          double2 p0 = __ldg(Pr + (int64_t)j * s);
+          double v0 = vs[j];
+          a0 += p0.x * v0; b0 += p0.y * v0;
+        }
       }
-      for (; j < cend; j += 8) a0 += __ldg(Pr + (int64_t)j * nf) * vs[j];
+      red[warp][2 * lane] = (a0 + a1) + (a2 + a3);
+      red[warp][2 * lane + 1] = (b0 + b1) + (b2 + b3);
+      __syncthreads();
+      if (warp < 2) {
+        int r = i0 + 32 * warp + lane;
+        int c = 32 * warp + lane;
+        if (r < r1) {
+          double tt = ((red[0][c] + red[1][c]) + (red[2][c] + red[3][c])) +
+                      ((red[4][c] + red[5][c]) + (red[6][c] + red[7][c]));
+          if (r < ns) b[cb + r] = tt;
+          else u[uoff[f] + (r - ns)] = v[r] - tt;
+        }
+      }
+      __syncthreads();
     }
-    red[warp][lane] = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
-    __syncthreads();
-    if (warp == 0 && row < r1) {
-      double t = ((red[0][lane] + red[1][lane]) + (red[2][lane] + red[3][lane])) +
-                 ((red[4][lane] + red[5][lane]) + (red[6][lane] + red[7][lane]));
-      if (row < ns) b[cb + row] = t;
-      else u[uoff[f] + (row - ns)] = v[row] - t;
-    }
-    __syncthreads();
   }
 }
 
@@ -219,44 +233,53 @@ k_bwd_gather(const int* fronts, const int* colbeg, const int* f_ns, const int* f
   for (int i = threadIdx.x; i < nf; i += blockDim.x) wf[i] = (i < ns) ? b[cb + i] : -q[sd[i - ns]];
 }
 
-// backward apply, task = (front, col_begin, col_end): x_j = P[:, j] . w_f
-__global__ void __launch_bounds__(kSolveThreads)
-k_bwd_apply(const int4* tasks, const int* colbeg, const int* f_ns, const int* f_nr,
-            const int64_t* loff, const int64_t* woff, const double* __restrict__ L,
+// backward apply, task = (front, col_begin, col_end): x_j = P[:, j] . w_f.
+// Persistent CTAs; one warp per column, lanes own row pairs (double2) from the
+// even row at or above the diagonal (the entry above it is an explicit zero).
+__global__ void __launch_bounds__(kSolveThreads, kApplyCtasPerSm)
+k_bwd_apply(const int4* tasks, int ntasks, const int* colbeg, const int* f_ns, const int* f_nr,
+            const int* f_ld, const int64_t* loff, const int64_t* woff, const double* __restrict__ L,
             const double* __restrict__ w, double* q) {
   __shared__ double sw[kVecCache];
-  int4 tk = tasks[blockIdx.x];
-  int f = tk.x, c0 = tk.y, c1 = tk.z;
-  int ns = f_ns[f], nf = ns + f_nr[f];
-  const double* P = L + loff[f];
-  const double* wf = w + woff[f];
-  int len = nf - c0;
-  const double* ws = wf + c0;
-  if (len <= kVecCache) {
-    for (int i = threadIdx.x; i < len; i += blockDim.x) sw[i] = wf[c0 + i];
-    ws = sw;
-  }
-  __syncthreads();
-  ws -= c0;  // index by absolute row
   int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int cb = colbeg[f];
-  for (int j = c0 + warp; j < c1; j += 8) {
-    const double* col = P + (int64_t)j * nf;
-    double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0, a6 = 0, a7 = 0;
-    int i = j + lane;
-    for (; i + 224 < nf; i += 256) {
-      a0 += __ldg(col + i) * ws[i];
-      a1 += __ldg(col + i + 32) * ws[i + 32];
-      a2 += __ldg(col + i + 64) * ws[i + 64];
-      a3 += __ldg(col + i + 96) * ws[i + 96];
-      a4 += __ldg(col + i + 128) * ws[i + 128];
-      a5 += __ldg(col + i + 160) * ws[i + 160];
-      a6 += __ldg(col + i + 192) * ws[i + 192];
-      a7 += __ldg(col + i + 224) * ws[i + 224];
+  for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
+    int4 tk = tasks[t];
+    int f = tk.x, c0 = tk.y, c1 = tk.z;
+    int ns = f_ns[f], nf = ns + f_nr[f], ld = f_ld[f];
+    const double* P = L + loff[f];
+    const double* wf = w + woff[f];
+    int e0 = c0 & ~1;        // even start
+    int len = ld - e0;       // includes the zero pad row
+    const double* ws = wf;
+    __syncthreads();
+    if (len <= kVecCache) {
+      for (int i = threadIdx.x; i < len; i += blockDim.x) sw[i] = wf[e0 + i];
+      ws = sw - e0;
     }
-    for (; i < nf; i += 32) a0 += __ldg(col + i) * ws[i];
-    double acc = warp_sum(((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7)));
-    if (lane == 0) q[cb + j] = acc;
+    __syncthreads();
+    int cb = colbeg[f];
+    for (int j = c0 + warp; j < c1; j += 8) {
+      const double2* col = reinterpret_cast<const double2*>(P + (int64_t)j * ld);
+      double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+      int i = (j & ~1) + 2 * lane;
+      for (; i + 192 < ld; i += 256) {
+        double2 p0 = __ldg(col + (i >> 1));
+        double2 p1 = __ldg(col + ((i + 64) >> 1));
+        double2 p2 = __ldg(col + ((i + 128) >> 1));
+        double2 p3 = __ldg(col + ((i + 192) >> 1));
+        a0 += p0.x * ws[i] + p0.y * ws[i + 1];
+        a1 += p1.x * ws[i + 64] + p1.y * ws[i + 65];
+        a2 += p2.x * ws[i + 128] + p2.y * ws[i + 129];
+        a3 += p3.x * ws[i + 192] + p3.y * ws[i + 193];
+      }
+      for (; i < ld; i += 64) {
+        double2 p0 = __ldg(col + (i >> 1));
+        a0 += p0.x * ws[i] + p0.y * ws[i + 1];
+      }
+      double acc = warp_sum((a0 + a1) + (a2 + a3));
+      if (lane == 0) q[cb + j] = acc;
+    }
+    (void)nf;
   }
 }
 
@@ -322,16 +345,17 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
   F.nlevels = S.nlevels;
   const int NF = S.nfronts;
   // ---- per-front metadata (DOF units)
-  std::vector<int> colbeg(NF), fns(NF), fnr(NF), cptr(S.child_ptr), clist(S.child_list);
+  std::vector<int> colbeg(NF), fns(NF), fnr(NF), fld(NF), cptr(S.child_ptr), clist(S.child_list);
   std::vector<int64_t> loff(NF + 1, 0), uoff(NF + 1, 0), woff(NF + 1, 0), sptr(NF + 1, 0);
   for (int f = 0; f < NF; ++f) {
     colbeg[f] = 3 * S.col_begin[f];
     fns[f] = 3 * (S.col_end[f] - S.col_begin[f]);
     fnr[f] = 3 * (int)(S.struct_ptr[f + 1] - S.struct_ptr[f]);
     int nf = fns[f] + fnr[f];
-    loff[f + 1] = loff[f] + (int64_t)nf * fns[f];
+    fld[f] = nf + (nf & 1);  // even leading dimension: 16-B aligned columns
+    loff[f + 1] = loff[f] + (int64_t)fld[f] * fns[f];
     uoff[f + 1] = uoff[f] + fnr[f];
-    woff[f + 1] = woff[f] + nf;
+    woff[f + 1] = woff[f] + fld[f];
     sptr[f + 1] = sptr[f] + fnr[f];
     F.max_nf = std::max(F.max_nf, nf);
   }
@@ -387,19 +411,19 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
         double ns = fns[f], nr = fnr[f];
         work += ns * (ns + 1) / 2 + nr * ns + nr;
       }
-      double T = std::max(work / (8.0 * 148), 4096.0);
+      double T = std::max(work / (16.0 * 148), 4096.0);
       for (int k = F.level_ptr[l]; k < F.level_ptr[l + 1]; ++k) {
         int f = lf[k];
         int ns = fns[f], nf = fns[f] + fnr[f];
         // forward rows
         int r0 = 0;
         double acc = 0;
-        for (int i0 = 0; i0 < nf; i0 += 32) {
-          int rows = std::min(32, nf - i0);
-          int cols = std::min(ns, i0 + 32);
+        for (int i0 = 0; i0 < nf; i0 += 64) {
+          int rows = std::min(64, nf - i0);
+          int cols = std::min(ns, i0 + 64);
           acc += (double)rows * std::max(cols, 1);
-          if (acc >= T || i0 + 32 >= nf) {
-            int r1 = std::min(nf, i0 + 32);
+          if (acc >= T || i0 + 64 >= nf) {
+            int r1 = std::min(nf, i0 + 64);
             ft.push_back(make_int4(f, r0, r1, 0));
             F.fwd_level_smem[l] = std::max(F.fwd_level_smem[l], std::min(ns, r1));
             r0 = r1;
@@ -474,6 +498,7 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
   F.f_colbeg = C.upload(colbeg.data(), NF);
   F.f_ns = C.upload(fns.data(), NF);
   F.f_nr = C.upload(fnr.data(), NF);
+  F.f_ld = C.upload(fld.data(), NF);
   F.f_loff = C.upload(loff.data(), NF + 1);
   F.f_uoff = C.upload(uoff.data(), NF + 1);
   F.f_woff = C.upload(woff.data(), NF + 1);
@@ -485,6 +510,7 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
   F.level_fronts = C.upload(lf.data(), NF);
   F.u = C.alloc<double>(uoff[NF]);
   F.w = C.alloc<double>(woff[NF]);
+  JGS2_CUDA(cudaMemsetAsync(F.w, 0, woff[NF] * sizeof(double), C.stream));
   F.L = C.alloc<double>(F.nnz_alloc);
   JGS2_CUDA(cudaMemsetAsync(F.L, 0, F.nnz_alloc * sizeof(double), C.stream));
   // vertex -> position map for the sweep kernels
@@ -525,8 +551,8 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
         if (it == ps + pn || *it != pi) throw Error(-1, "symbolic: entry outside front structure");
         li = fns[f] + 3 * (int)(it - ps);
       }
-      bdst[k] = loff[f] + (int64_t)lj * nf + li;
-      bld[k] = nf;
+      bdst[k] = loff[f] + (int64_t)lj * fld[f] + li;
+      bld[k] = fld[f];
     }
   }
   int* d_brow = C.upload(brow.data(), nblocks);
@@ -585,7 +611,7 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
   std::vector<double*> Ubuf(NF, nullptr);
   const double one = 1.0, mone = -1.0;
   for (int f = 0; f < NF; ++f) {
-    int ns = fns[f], nr = fnr[f], nf = ns + nr;
+    int ns = fns[f], nr = fnr[f], nf = fld[f];  // nf: leading dimension below
     double* Pf = F.L + loff[f];
     if (nr > 0) {
       JGS2_CUDA(cudaMallocAsync(&Ubuf[f], (size_t)nr * nr * sizeof(double), C.stream));
@@ -654,9 +680,10 @@ void factor_solve_launches(Ctx& C) {
                                                                F.asm_cp + o, F.asm_src, C.b, F.u, F.w);
     C.check_launch();
     int nt = F.fwd_level_ptr[l + 1] - F.fwd_level_ptr[l];
-    k_fwd_apply<<<nt, kSolveThreads, 0, C.stream>>>(F.fwd_tasks + F.fwd_level_ptr[l], F.f_colbeg,
-                                                    F.f_ns, F.f_nr, F.f_loff, F.f_uoff, F.f_woff,
-                                                    F.L, F.w, C.b, F.u);
+    int g = std::min(nt, 148 * kApplyCtasPerSm);
+    k_fwd_apply<<<g, kSolveThreads, 0, C.stream>>>(F.fwd_tasks + F.fwd_level_ptr[l], nt, F.f_colbeg,
+                                                   F.f_ns, F.f_nr, F.f_ld, F.f_loff, F.f_uoff,
+                                                   F.f_woff, F.L, F.w, C.b, F.u);
     C.check_launch();
   }
   for (int l = F.nlevels - 1; l >= 0; --l) {
@@ -667,8 +694,10 @@ void factor_solve_launches(Ctx& C) {
     k_bwd_gather_flat<<<grid_for(ng), kBlock, 0, C.stream>>>(ng, F.gat_dst + o, F.gat_src + o, C.b,
                                                              C.q, F.w);
     C.check_launch();
-    k_bwd_apply<<<nt, kSolveThreads, 0, C.stream>>>(F.bwd_tasks + F.bwd_level_ptr[l], F.f_colbeg,
-                                                    F.f_ns, F.f_nr, F.f_loff, F.f_woff, F.L, F.w, C.q);
+    int gb = std::min(nt, 148 * kApplyCtasPerSm);
+    k_bwd_apply<<<gb, kSolveThreads, 0, C.stream>>>(F.bwd_tasks + F.bwd_level_ptr[l], nt, F.f_colbeg,
+                                                    F.f_ns, F.f_nr, F.f_ld, F.f_loff, F.f_woff, F.L,
+                                                    F.w, C.q);
     C.check_launch();
   }
 }
