@@ -95,6 +95,8 @@ typedef struct jgs2_sweep_info {
   double energy;           /* total_energy at the new x (track_energy) */
   int32_t halvings;        /* global backtrack halvings */
   int32_t n_pairs;         /* active pairs at the sweep start */
+  int32_t n_indefinite;    /* cubature elements whose Hessian needed projection */
+  int32_t pad_;
 } jgs2_sweep_info;
 
 typedef struct jgs2_factor_info {

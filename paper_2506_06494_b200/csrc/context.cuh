@@ -126,6 +126,11 @@ struct Ctx {
   double* crest = nullptr;     // nv*9 rest constant C_v
   int* uniq = nullptr;         // nuniq element ids
   double* mplus = nullptr;     // nuniq*45 per-sweep projected reduced Hessians
+  int* hess_count = nullptr;   // indefinite-element count (pass 1 -> pass 2)
+  int* hess_list = nullptr;    // compacted indefinite elements
+  cudaStream_t stream2 = nullptr;  // side stream for the element-Hessian passes
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool hess_pending = false;
   // retained rows CSR for contact coupling rows (local_solver.py:85-112)
   int* vr_ptr = nullptr;       // nv+1
   int* vr_keys = nullptr;

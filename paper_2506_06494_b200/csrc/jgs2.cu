@@ -24,6 +24,10 @@ jgs2::Ctx::~Ctx() {
   if (tstop) cudaEventDestroy(tstop);
   if (cublas) cublasDestroy(cublas);
   if (cusolver) cusolverDnDestroy(cusolver);
+  if (stream2) cudaStreamSynchronize(stream2);
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
+  if (stream2) cudaStreamDestroy(stream2);
   if (fac.graph_exec) cudaGraphExecDestroy(fac.graph_exec);
   if (stream) cudaStreamDestroy(stream);
 }
@@ -136,14 +140,43 @@ void collect(Ctx& C) {
   C.phase_end();
 }
 
+// Element Hessians at x on the side stream: compute-bound FP64 work that
+// overlaps the memory-bound vertex pass + collect on the main stream
+// (independent: H_cur depends on x only); joined before k_local.
+void hessians_async(Ctx& C) {
+  if (C.nuniq == 0 || C.hess_pending) return;
+  JGS2_CUDA(cudaEventRecord(C.ev_fork, C.stream));
+  JGS2_CUDA(cudaStreamWaitEvent(C.stream2, C.ev_fork, 0));
+  C.phase_bytes[3] += bytes_cub(C);
+  cudaEvent_t a = nullptr;
+  if (C.profiling) {
+    a = C.take_event();
+    JGS2_CUDA(cudaEventRecord(a, C.stream2));
+  }
+  launch_element_mplus(C.nuniq, C.uniq, C.x, C.tets, C.dminv, C.eprops, C.mplus, C.hess_count,
+                       C.hess_list, C.stream2);
+  C.launches += 2;
+  C.check_launch();
+  if (C.profiling) {
+    cudaEvent_t b = C.take_event();
+    JGS2_CUDA(cudaEventRecord(b, C.stream2));
+    C.phase_launch[3] += 2;
+    C.pending.push_back({3, {a, b}});
+  }
+  JGS2_CUDA(cudaEventRecord(C.ev_join, C.stream2));
+  C.hess_pending = true;
+}
+
+void hessians_join(Ctx& C) {
+  if (!C.hess_pending) return;
+  JGS2_CUDA(cudaStreamWaitEvent(C.stream, C.ev_join, 0));
+  C.hess_pending = false;
+}
+
 void local_systems(Ctx& C, double* A_out, double* g_out, double* corr_out) {
   DevModel m = devmodel(C);
-  if (C.nuniq > 0) {
-    C.phase_begin(3, bytes_cub(C));
-    launch_element_mplus(C.nuniq, C.uniq, C.x, C.tets, C.dminv, C.eprops, C.mplus, C.stream);
-    C.check_launch();
-    C.phase_end();
-  }
+  hessians_async(C);  // no-op if already in flight
+  hessians_join(C);
   C.phase_begin(4, bytes_local(C));
   JGS2_CUDA(cudaMemsetAsync(C.ls_cnt, 0, (C.max_halvings + 2) * sizeof(int), C.stream));
   JGS2_CUDA(cudaMemsetAsync(C.ls_max, 0, (C.max_halvings + 2) * sizeof(unsigned long long), C.stream));
@@ -231,8 +264,13 @@ void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
   C.phase_end();
   if (C.track_energy && !have_trial_energy) launch_energy(C, nullptr, 0.0, R_ENERGY);
   JGS2_CUDA(cudaMemcpyAsync(C.h_res, C.res, R_NSLOTS * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+  int n_indef = 0;
+  if (C.nuniq > 0)
+    JGS2_CUDA(cudaMemcpyAsync(C.h_res + R_NSLOTS + 1, C.hess_count, sizeof(int), cudaMemcpyDeviceToHost, C.stream));
   C.sync();
+  if (C.nuniq > 0) memcpy(&n_indef, C.h_res + R_NSLOTS + 1, sizeof(int));
   if (info) {
+    info->n_indefinite = n_indef;
     info->grad_sq = C.h_res[R_GRADSQ];
     info->grad_norm = std::sqrt(C.h_res[R_GRADSQ]);
     info->max_local_step = C.h_res[R_DXMAX];
@@ -272,7 +310,11 @@ jgs2_ctx* jgs2_create(int32_t device) {
     JGS2_CUDA(cudaMemset(C.counters, 0, R_NSLOTS * sizeof(unsigned)));
     JGS2_CUDA(cudaMemset(C.res, 0, R_NSLOTS * sizeof(double)));
     JGS2_CUDA(cudaMallocHost(&C.h_res, 2 * R_NSLOTS * sizeof(double)));
-    cudaFuncSetAttribute(k_element_mplus, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    C.hess_count = C.alloc<int>(2);
+    JGS2_CUDA(cudaStreamCreateWithFlags(&C.stream2, cudaStreamNonBlocking));
+    JGS2_CUDA(cudaEventCreateWithFlags(&C.ev_fork, cudaEventDisableTiming));
+    JGS2_CUDA(cudaEventCreateWithFlags(&C.ev_join, cudaEventDisableTiming));
+    cudaFuncSetAttribute(k_hess_pass2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kHessSmemBytes);
 
   } catch (...) {
@@ -442,6 +484,7 @@ int32_t jgs2_set_precompute(jgs2_ctx* ctx, const jgs2_precompute* p, const jgs2_
     C.nslots = 0;
     for (int e : cub_e) C.nslots += (e >= 0);
     C.mplus = C.alloc<double>(45 * (size_t)std::max(C.nuniq, 1));
+    C.hess_list = C.alloc<int>(std::max(C.nuniq, 1));
     C.crest = C.alloc<double>(9 * (size_t)nv);
     JGS2_CUDA(cudaMemsetAsync(C.crest, 0, 9 * (size_t)nv * sizeof(double), C.stream));
     C.ls_max = C.alloc<unsigned long long>(C.max_halvings + 2);
@@ -470,7 +513,8 @@ int32_t jgs2_set_precompute(jgs2_ctx* ctx, const jgs2_precompute* p, const jgs2_
     if (C.nuniq > 0) {
       DevModel m = devmodel(C);
       // pos is needed by devmodel consumers only after factoring; not used here
-      launch_element_mplus(C.nuniq, C.uniq, C.rest, C.tets, C.dminv, C.eprops, C.mplus, C.stream);
+      launch_element_mplus(C.nuniq, C.uniq, C.rest, C.tets, C.dminv, C.eprops, C.mplus, C.hess_count,
+                           C.hess_list, C.stream);
       C.check_launch();
       double* Rid = nullptr;
       JGS2_CUDA(cudaMallocAsync(&Rid, 9 * (size_t)nv * sizeof(double), C.stream));

@@ -289,7 +289,8 @@ class LocalSolver:
                 "max_local_step": float(inf.max_local_step),
                 "grad_norm": float(inf.grad_norm), "grad_sq": float(inf.grad_sq),
                 "dx_norm": float(inf.dx_norm), "energy": float(inf.energy),
-                "halvings": int(inf.halvings), "n_pairs": int(inf.n_pairs)}
+                "halvings": int(inf.halvings), "n_pairs": int(inf.n_pairs),
+                "n_indefinite": int(inf.n_indefinite)}
 
     # ------------------------------------------------------------ hot path
     def sweep(self, state, rotations=None):
