@@ -1,0 +1,164 @@
+// GPU uniform-grid broadphase for vertex-triangle proximity.
+//
+// Reference: contact.point_distances / feasibility_step_cap test ALL
+// (surface vertex, surface triangle) pairs of distinct bodies by brute force
+// (contact.py:229-239, assembly.py:279-290). Here every surface triangle is
+// inserted into each grid cell its AABB, inflated by the query radius r,
+// overlaps; a vertex only visits the triangles of its own cell. Any
+// triangle within distance < r of the vertex contains the vertex in its
+// inflated AABB, so the candidate set is a superset of the exact set and
+// the (unchanged, reference-rounding) narrowphase yields the identical pair
+// set. Entries are radix-sorted by cell key (stable, so the triangles of a
+// cell stay in ascending id order): candidates arrive in the reference's
+// row-major (vertex, triangle) order without a per-vertex sort.
+#pragma once
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "context.cuh"
+#include "geometry.cuh"
+
+namespace jgs2 {
+
+constexpr long long kCellOff = 1LL << 20;
+
+__device__ __forceinline__ long long cell_coord(double v, double inv_cell) {
+  long long c = (long long)floor(v * inv_cell);
+  c = c < -kCellOff + 1 ? -kCellOff + 1 : (c > kCellOff - 2 ? kCellOff - 2 : c);
+  return c;
+}
+__device__ __forceinline__ unsigned long long cell_key(long long ix, long long iy, long long iz) {
+  return ((unsigned long long)(ix + kCellOff) << 42) | ((unsigned long long)(iy + kCellOff) << 21) |
+         (unsigned long long)(iz + kCellOff);
+}
+
+struct TriGridDev {
+  const unsigned long long* keys;  // sorted cell keys
+  const int* tris;                 // triangle ids, ascending within a key
+  long long n;
+  double inv_cell;
+};
+
+__device__ __forceinline__ void tri_bounds(const int* st, int t, const double* x, const double* dx,
+                                           double gamma, double r, double inv_cell, long long* lo,
+                                           long long* hi) {
+  double a[3], b[3], c[3];
+  load_pos(x, dx, gamma, st[3 * t], a);
+  load_pos(x, dx, gamma, st[3 * t + 1], b);
+  load_pos(x, dx, gamma, st[3 * t + 2], c);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double mn = fmin(a[k], fmin(b[k], c[k])) - r;
+    double mx = fmax(a[k], fmax(b[k], c[k])) + r;
+    lo[k] = cell_coord(mn, inv_cell);
+    hi[k] = cell_coord(mx, inv_cell);
+  }
+}
+
+__global__ void k_grid_count(int nst, const int* st, const double* x, const double* dx, double gamma,
+                             double r, double inv_cell, long long* counts) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > nst) return;
+  if (t == nst) { counts[t] = 0; return; }
+  long long lo[3], hi[3];
+  tri_bounds(st, t, x, dx, gamma, r, inv_cell, lo, hi);
+  counts[t] = (hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1) * (hi[2] - lo[2] + 1);
+}
+
+__global__ void k_grid_write(int nst, const int* st, const double* x, const double* dx, double gamma,
+                             double r, double inv_cell, const long long* off, unsigned long long* keys,
+                             int* tris) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nst) return;
+  long long lo[3], hi[3];
+  tri_bounds(st, t, x, dx, gamma, r, inv_cell, lo, hi);
+  long long o = off[t];
+  for (long long i = lo[0]; i <= hi[0]; ++i)
+    for (long long j = lo[1]; j <= hi[1]; ++j)
+      for (long long k = lo[2]; k <= hi[2]; ++k) {
+        keys[o] = cell_key(i, j, k);
+        tris[o] = t;
+        ++o;
+      }
+}
+
+// [first, last) of entries with this key
+__device__ __forceinline__ void grid_range(const TriGridDev& g, unsigned long long key, long long* first,
+                                           long long* last) {
+  long long lo = 0, hi = g.n;
+  while (lo < hi) {
+    long long mid = (lo + hi) >> 1;
+    if (g.keys[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  *first = lo;
+  hi = g.n;
+  while (lo < hi) {
+    long long mid = (lo + hi) >> 1;
+    if (g.keys[mid] <= key) lo = mid + 1; else hi = mid;
+  }
+  *last = lo;
+}
+
+__device__ __forceinline__ unsigned long long point_key(const double* p, double inv_cell) {
+  return cell_key(cell_coord(p[0], inv_cell), cell_coord(p[1], inv_cell), cell_coord(p[2], inv_cell));
+}
+
+inline TriGridDev grid_dev(const TriGrid& g) { return TriGridDev{g.keys_b, g.tris_b, g.n, 1.0 / g.cell}; }
+
+inline void tri_grid_free(TriGrid& g) {
+  cudaFree(g.counts); cudaFree(g.off); cudaFree(g.keys_a); cudaFree(g.keys_b);
+  cudaFree(g.tris_a); cudaFree(g.tris_b); cudaFree(g.temp);
+  g = TriGrid();
+}
+
+// Build the grid of surface triangles at x + gamma*dx inflated by r.
+// One host sync (the entry count).
+inline void tri_grid_build(Ctx& C, TriGrid& g, const double* x, const double* dx, double gamma, double r,
+                           double cell) {
+  int nst = C.nst;
+  g.cell = cell;
+  if (!g.counts) {
+    JGS2_CUDA(cudaMalloc(&g.counts, (nst + 1) * sizeof(long long)));
+    JGS2_CUDA(cudaMalloc(&g.off, (nst + 1) * sizeof(long long)));
+  }
+  k_grid_count<<<grid_for(nst + 1), kBlock, 0, C.stream>>>(nst, C.st, x, dx, gamma, r, 1.0 / cell, g.counts);
+  C.check_launch();
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, g.counts, g.off, nst + 1, C.stream);
+  if (tb > g.temp_bytes) {
+    cudaFree(g.temp);
+    JGS2_CUDA(cudaMalloc(&g.temp, tb));
+    g.temp_bytes = tb;
+  }
+  JGS2_CUDA(cub::DeviceScan::ExclusiveSum(g.temp, tb, g.counts, g.off, nst + 1, C.stream));
+  ++C.launches;
+  long long total = 0;
+  JGS2_CUDA(cudaMemcpyAsync(&total, g.off + nst, sizeof(long long), cudaMemcpyDeviceToHost, C.stream));
+  C.sync();
+  if (total > g.cap) {
+    cudaFree(g.keys_a); cudaFree(g.keys_b); cudaFree(g.tris_a); cudaFree(g.tris_b);
+    long long cap = std::max<long long>(total + total / 2, 1024);
+    JGS2_CUDA(cudaMalloc(&g.keys_a, cap * sizeof(unsigned long long)));
+    JGS2_CUDA(cudaMalloc(&g.keys_b, cap * sizeof(unsigned long long)));
+    JGS2_CUDA(cudaMalloc(&g.tris_a, cap * sizeof(int)));
+    JGS2_CUDA(cudaMalloc(&g.tris_b, cap * sizeof(int)));
+    g.cap = cap;
+  }
+  g.n = total;
+  k_grid_write<<<grid_for(nst), kBlock, 0, C.stream>>>(nst, C.st, x, dx, gamma, r, 1.0 / cell, g.off,
+                                                       g.keys_a, g.tris_a);
+  C.check_launch();
+  size_t sb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, sb, g.keys_a, g.keys_b, g.tris_a, g.tris_b, (int)total, 0, 63,
+                                  C.stream);
+  if (sb > g.temp_bytes) {
+    cudaFree(g.temp);
+    JGS2_CUDA(cudaMalloc(&g.temp, sb));
+    g.temp_bytes = sb;
+  }
+  JGS2_CUDA(cub::DeviceRadixSort::SortPairs(g.temp, sb, g.keys_a, g.keys_b, g.tris_a, g.tris_b, (int)total,
+                                            0, 63, C.stream));
+  ++C.launches;
+}
+
+}  // namespace jgs2

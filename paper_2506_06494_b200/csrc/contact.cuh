@@ -11,6 +11,7 @@
 #include "context.cuh"
 #include "sweep.cuh"
 #include "geometry.cuh"
+#include "broadphase.cuh"
 
 namespace jgs2 {
 
@@ -25,9 +26,9 @@ struct ContactDev {
 };
 
 // Pass 1: per surface vertex, counts of plane hits (per plane) and
-// cross-body triangle hits (brute force over all surface triangles).
-__global__ void k_pair_count(ContactDev cd, const double* x, const double* dx, double gamma,
-                             int* cnt /* (nplanes+1) x nsv */) {
+// cross-body triangle hits (grid candidates, ascending triangle id).
+__global__ void k_pair_count(ContactDev cd, TriGridDev g, int use_grid, const double* x, const double* dx,
+                             double gamma, int* cnt /* (nplanes+1) x nsv */) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= cd.nsv) return;
   int v = cd.sv[i];
@@ -37,7 +38,11 @@ __global__ void k_pair_count(ContactDev cd, const double* x, const double* dx, d
     cnt[pl * cd.nsv + i] = (plane_dist(p, cd.planes + 6 * pl) < cd.dhat) ? 1 : 0;
   int hits = 0;
   int bv = cd.vbody[v];
-  for (int t = 0; t < cd.nst; ++t) {
+  long long q0 = 0, q1 = 0;
+  if (use_grid) grid_range(g, point_key(p, g.inv_cell), &q0, &q1);
+  else q1 = cd.nst;
+  for (long long q = q0; q < q1; ++q) {
+    int t = use_grid ? g.tris[q] : (int)q;
     if (cd.tbody[t] == bv) continue;
     double a[3], b[3], c[3], bary[3];
     load_pos(x, dx, gamma, cd.st[3 * t], a);
@@ -87,8 +92,8 @@ __global__ void k_scan_excl(const int* in, int* out, int n) {
 }
 
 // Pass 2: write pair rows in the reference order (contact.py:224-239).
-__global__ void k_pair_write(ContactDev cd, const double* x, const double* dx, double gamma,
-                             const int* off, int cap, double* rows, int* flag) {
+__global__ void k_pair_write(ContactDev cd, TriGridDev g, int use_grid, const double* x, const double* dx,
+                             double gamma, const int* off, int cap, double* rows, int* flag) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= cd.nsv) return;
   int v = cd.sv[i];
@@ -107,7 +112,11 @@ __global__ void k_pair_write(ContactDev cd, const double* x, const double* dx, d
   }
   int o = off[cd.nplanes * cd.nsv + i];
   int bv = cd.vbody[v];
-  for (int t = 0; t < cd.nst; ++t) {
+  long long q0 = 0, q1 = 0;
+  if (use_grid) grid_range(g, point_key(p, g.inv_cell), &q0, &q1);
+  else q1 = cd.nst;
+  for (long long q = q0; q < q1; ++q) {
+    int t = use_grid ? g.tris[q] : (int)q;
     if (cd.tbody[t] == bv) continue;
     double a[3], b[3], c[3], bary[3];
     load_pos(x, dx, gamma, cd.st[3 * t], a);
@@ -442,7 +451,17 @@ __global__ void k_cap_planes(ContactDev cd, const double* x, const double* dx, d
   }
   grid_reduce<OP_MIN>(mn, partials, counter, out);
 }
-__global__ void k_cap_tris(ContactDev cd, const double* x, const double* dx, double* partials,
+// max_v |dx_v| over surface vertices (query radius of the cap grid)
+__global__ void k_sv_maxstep(ContactDev cd, const double* dx, double* partials, unsigned* counter,
+                             double* out) {
+  double mx = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cd.nsv; i += gridDim.x * blockDim.x)
+    mx = fmax(mx, norm3_np(dx + 3 * cd.sv[i]));
+  grid_reduce<OP_MAX>(mx, partials, counter, out);
+}
+
+// min over cross-body (vertex, triangle) candidates of dist / rate
+__global__ void k_cap_tris(ContactDev cd, TriGridDev g, const double* x, const double* dx, double* partials,
                            unsigned* counter, double* out) {
   double mn = INFINITY;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cd.nsv; i += gridDim.x * blockDim.x) {
@@ -450,7 +469,10 @@ __global__ void k_cap_tris(ContactDev cd, const double* x, const double* dx, dou
     double p[3] = {x[3 * v], x[3 * v + 1], x[3 * v + 2]};
     double sp = norm3_np(dx + 3 * v);
     int bv = cd.vbody[v];
-    for (int t = 0; t < cd.nst; ++t) {
+    long long q0, q1;
+    grid_range(g, point_key(p, g.inv_cell), &q0, &q1);
+    for (long long q = q0; q < q1; ++q) {
+      int t = g.tris[q];
       if (cd.tbody[t] == bv) continue;
       int a0 = cd.st[3 * t], a1 = cd.st[3 * t + 1], a2 = cd.st[3 * t + 2];
       double st = fmax(fmax(norm3_np(dx + 3 * a0), norm3_np(dx + 3 * a1)), norm3_np(dx + 3 * a2));
@@ -490,7 +512,12 @@ void contact_setup(Ctx& C, const jgs2_model* md) {
     }
   C.planes = C.upload(C.h_planes.data(), C.h_planes.size());
   std::vector<int> sv(C.nsv), st(3 * (size_t)C.nst), vb(C.nv), tb(C.nst);
-  for (int i = 0; i < C.nsv; ++i) sv[i] = (int)md->surface_vertices[i];
+  C.h_surface.assign(C.nv, 0);
+  for (int i = 0; i < C.nsv; ++i) {
+    sv[i] = (int)md->surface_vertices[i];
+    if (sv[i] < 0 || sv[i] >= C.nv) throw Error(-1, "surface vertex out of range");
+    C.h_surface[sv[i]] = 1;
+  }
   for (size_t i = 0; i < st.size(); ++i) st[i] = (int)md->surface_tris[i];
   for (int i = 0; i < C.nv; ++i) vb[i] = md->vertex_body ? (int)md->vertex_body[i] : 0;
   for (int i = 0; i < C.nst; ++i) tb[i] = md->surface_tri_body ? (int)md->surface_tri_body[i] : 0;
@@ -504,6 +531,20 @@ void contact_setup(Ctx& C, const jgs2_model* md) {
   C.vp_ptr = C.alloc<int>(C.nv + 1);
   C.flag_d = C.alloc<int>(2);
   C.npairs_d = C.alloc<int>(2);
+  // grid cell: 2x the mean surface-triangle edge at rest, at least 2 dhat
+  double el = 0.0;
+  for (int t = 0; t < C.nst; ++t)
+    for (int k = 0; k < 3; ++k) {
+      int a = st[3 * t + k], b = st[3 * t + (k + 1) % 3];
+      double d2 = 0.0;
+      for (int c = 0; c < 3; ++c) {
+        double dd = C.h_rest[3 * (size_t)a + c] - C.h_rest[3 * (size_t)b + c];
+        d2 += dd * dd;
+      }
+      el += std::sqrt(d2);
+    }
+  el = C.nst > 0 ? el / (3.0 * C.nst) : 1.0;
+  C.grid_cell = std::max(2.0 * el, 2.0 * C.dhat);
 }
 
 void ensure_pair_capacity(Ctx& C, int64_t need) {
@@ -517,21 +558,43 @@ void ensure_pair_capacity(Ctx& C, int64_t need) {
   C.cap_pairs = cap;
 }
 
+// exclusive scan of n ints into out[0..n] (out[n] = total), CUB device scan
+void scan_ints(Ctx& C, int* in, int* out, int n) {
+  JGS2_CUDA(cudaMemsetAsync(in + n, 0, sizeof(int), C.stream));
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n + 1, C.stream);
+  if (tb > C.scan_temp_bytes) {
+    C.scan_temp = C.alloc<char>(tb);
+    C.scan_temp_bytes = tb;
+  }
+  JGS2_CUDA(cub::DeviceScan::ExclusiveSum(C.scan_temp, tb, in, out, n + 1, C.stream));
+  ++C.launches;
+}
+
+bool use_tri_grid(const Ctx& C) { return C.nbodies > 1 && C.nst > 0; }
+
 // Detect active pairs at x + gamma*dx into the pair table; sets C.npairs
 // (host sync) and the infeasibility flag.
 void contact_find_pairs(Ctx& C, const double* x, const double* dx, double gamma) {
   ContactDev cd = contactdev(C);
   int n = (C.nplanes + 1) * C.nsv;
   JGS2_CUDA(cudaMemsetAsync(C.flag_d, 0, sizeof(int), C.stream));
-  k_pair_count<<<grid_for(C.nsv, 128), 128, 0, C.stream>>>(cd, x, dx, gamma, C.pair_count_sv);
+  int ug = use_tri_grid(C) ? 1 : 0;
+  TriGridDev gd{nullptr, nullptr, 0, 1.0};
+  if (ug) {
+    tri_grid_build(C, C.pair_grid, x, dx, gamma, C.dhat * (1.0 + 1e-6) + 1e-300, C.grid_cell);
+    gd = grid_dev(C.pair_grid);
+  } else {
+    cd.nst = 0;  // single body: no cross-body triangle pairs
+  }
+  k_pair_count<<<grid_for(C.nsv, 128), 128, 0, C.stream>>>(cd, gd, ug, x, dx, gamma, C.pair_count_sv);
   C.check_launch();
-  k_scan_excl<<<1, 1024, 0, C.stream>>>(C.pair_count_sv, C.pair_off_sv, n);
-  C.check_launch();
+  scan_ints(C, C.pair_count_sv, C.pair_off_sv, n);
   int total = 0;
   JGS2_CUDA(cudaMemcpyAsync(&total, C.pair_off_sv + n, sizeof(int), cudaMemcpyDeviceToHost, C.stream));
   C.sync();
   ensure_pair_capacity(C, total);
-  k_pair_write<<<grid_for(C.nsv, 128), 128, 0, C.stream>>>(cd, x, dx, gamma, C.pair_off_sv,
+  k_pair_write<<<grid_for(C.nsv, 128), 128, 0, C.stream>>>(cd, gd, ug, x, dx, gamma, C.pair_off_sv,
                                                            (int)C.cap_pairs, C.pairs, C.flag_d);
   C.check_launch();
   C.npairs = total;
@@ -566,8 +629,7 @@ void contact_add_gradients(Ctx& C) {
   JGS2_CUDA(cudaMemsetAsync(C.vp_cnt, 0, (C.nv + 1) * sizeof(int), C.stream));
   k_vp_count<<<grid_for(C.npairs), kBlock, 0, C.stream>>>(C.npairs, C.pairs, C.vp_cnt);
   C.check_launch();
-  k_scan_excl<<<1, 1024, 0, C.stream>>>(C.vp_cnt, C.vp_ptr, C.nv);
-  C.check_launch();
+  scan_ints(C, C.vp_cnt, C.vp_ptr, C.nv);
   JGS2_CUDA(cudaMemsetAsync(C.vp_cnt, 0, (C.nv + 1) * sizeof(int), C.stream));
   k_vp_fill<<<grid_for(C.npairs), kBlock, 0, C.stream>>>(C.npairs, C.pairs, C.vp_ptr, C.vp_cnt, C.vp_list);
   C.check_launch();
@@ -589,9 +651,21 @@ double contact_step_cap(Ctx& C, const double* x, const double* dx) {
     C.sync();
     if (std::isfinite(m)) cap = std::min(cap, 0.9 * m);
   }
-  if (C.nbodies > 1 && C.nst > 0) {
-    k_cap_tris<<<red_grid(C.nsv), kBlock, 0, C.stream>>>(cd, x, dx, C.partials + R_CAP * kMaxPartials,
+  if (use_tri_grid(C)) {
+    // only pairs with dist < max rate / 0.9 can lower the cap below 1, and
+    // rate <= 2 max|dx|: a grid inflated by that radius is exact.
+    k_sv_maxstep<<<red_grid(C.nsv), kBlock, 0, C.stream>>>(cd, dx, C.partials + R_CAP * kMaxPartials,
                                                            C.counters + R_CAP, C.res + R_CAP);
+    C.check_launch();
+    double M = 0;
+    JGS2_CUDA(cudaMemcpyAsync(&M, C.res + R_CAP, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    C.sync();
+    if (!(M > 0)) return std::max(cap, 0.0);
+    double r = 2.0 * M / 0.9 * (1.0 + 1e-6);
+    tri_grid_build(C, C.cap_grid, x, nullptr, 0.0, r, std::max(C.grid_cell, r));
+    k_cap_tris<<<red_grid(C.nsv), kBlock, 0, C.stream>>>(cd, grid_dev(C.cap_grid), x, dx,
+                                                         C.partials + R_CAP * kMaxPartials,
+                                                         C.counters + R_CAP, C.res + R_CAP);
     C.check_launch();
     double m = 0;
     JGS2_CUDA(cudaMemcpyAsync(&m, C.res + R_CAP, sizeof(double), cudaMemcpyDeviceToHost, C.stream));

@@ -42,6 +42,18 @@ enum ResSlot {
   R_NSLOTS = 8
 };
 
+// Broadphase grid buffers (see broadphase.cuh; grow on demand).
+struct TriGrid {
+  long long cap = 0, n = 0;
+  long long* counts = nullptr;  // nst + 1
+  long long* off = nullptr;
+  unsigned long long *keys_a = nullptr, *keys_b = nullptr;
+  int *tris_a = nullptr, *tris_b = nullptr;
+  void* temp = nullptr;
+  size_t temp_bytes = 0;
+  double cell = 0.0;
+};
+
 // Device-side factor of the free-vertex rest Hessian (supernodal, ND order).
 struct Factor {
   bool ready = false;
@@ -167,6 +179,7 @@ struct Ctx {
   double* planes = nullptr;    // nplanes*6 (point, normal)
   std::vector<double> h_planes;
   int* sv = nullptr;           // surface vertices
+  std::vector<uint8_t> h_surface;  // host surface-vertex mask
   int* st = nullptr;           // surface tris *3
   int* vbody = nullptr;        // nv
   int* tbody = nullptr;        // nst
@@ -184,6 +197,10 @@ struct Ctx {
   double* pair_h = nullptr;    // per pair 144 projected Hessian
   double* pair_e = nullptr;    // per pair barrier energy
   int* flag_d = nullptr;       // infeasibility flag
+  double grid_cell = 1.0;      // broadphase cell size
+  TriGrid pair_grid, cap_grid;
+  void* scan_temp = nullptr;   // CUB scan workspace
+  size_t scan_temp_bytes = 0;
 
   // measurement: per-phase CUDA-event intervals (accumulated at sync points)
   bool profiling = false;

@@ -243,80 +243,80 @@ __device__ void sym_eig9_shared(double* V, double* d, double* e) {
 #undef EE
 }
 
-// Pass 1 (high occupancy, no shared memory): closed-form M per element; a
-// positive-definite M is final (PSD(M) = M); an indefinite one is stored and
-// its index appended to a compacted list for pass 2. The list order depends
-// on atomics but every element's result depends only on its own data, so
-// the output is deterministic.
+// One thread per element: closed-form M, LDL^T inertia test, and (when
+// indefinite) the tred2/tql2 projection on per-thread interleaved shared
+// memory. The number of indefinite elements is accumulated with one
+// warp-aggregated atomic per warp (diagnostic only; results do not depend
+// on it).
 __global__ void __launch_bounds__(kHessThreads)
-k_hess_pass1(int n, const int* elems, const double* __restrict__ xs, const int4* __restrict__ tets,
-             const double* __restrict__ dminv, const double4* __restrict__ eprops, double* mplus,
-             int* count, int* list) {
-  int u = blockIdx.x * blockDim.x + threadIdx.x;
-  if (u >= n) return;
-  int e = elems ? elems[u] : u;
-  double D[9];
-#pragma unroll
-  for (int i = 0; i < 9; ++i) D[i] = __ldg(dminv + 9 * (size_t)e + i);
-  int4 t = __ldg(tets + e);
-  double x0[3], x1[3], x2[3], x3[3];
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    x0[c] = __ldg(xs + 3 * t.x + c); x1[c] = __ldg(xs + 3 * t.y + c);
-    x2[c] = __ldg(xs + 3 * t.z + c); x3[c] = __ldg(xs + 3 * t.w + c);
-  }
-  double F[9];
-  deformation_gradient(x0, x1, x2, x3, D, F);
-  double4 ep = eprops[e];
-  double Mp[45];
-  reduced_hessian_closed(F, D, ep.x, snh_const(ep.y, ep.z), Mp);
-  double* o = mplus + 45 * (size_t)u;
-#pragma unroll
-  for (int i = 0; i < 45; ++i) o[i] = Mp[i];
-  if (!is_pos_def9(Mp)) list[atomicAdd(count, 1)] = u;
-}
-
-// Pass 2: eigen-projection of the indefinite elements (tred2 + tql2 on
-// per-thread interleaved shared memory), M+ = Q max(L,0) Q^T in place.
-__global__ void __launch_bounds__(kHessThreads)
-k_hess_pass2(const int* count, const int* list, double* mplus) {
+k_element_mplus(int n, const int* elems, const double* __restrict__ xs, const int4* __restrict__ tets,
+                const double* __restrict__ dminv, const double4* __restrict__ eprops, double* mplus,
+                int* count) {
   extern __shared__ double hsm[];
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= *count) return;
-  int u = list[k];
-  double* Vs = hsm + threadIdx.x;
-  double* ds = hsm + 81 * kHessThreads + threadIdx.x;
-  double* es = hsm + 90 * kHessThreads + threadIdx.x;
-  double* o = mplus + 45 * (size_t)u;
-  for (int i = 0; i < 9; ++i)
-    for (int j = 0; j <= i; ++j) {
-      double v = o[JGS2_PK(i, j)];
-      Vs[(9 * i + j) * kHessThreads] = v;
-      Vs[(9 * j + i) * kHessThreads] = v;
-    }
-  sym_eig9_shared<kHessThreads>(Vs, ds, es);
-  double lam[9];
+  int u = blockIdx.x * blockDim.x + threadIdx.x;
+  bool active = u < n;
+  bool indef = false;
+  if (active) {
+    int e = elems ? elems[u] : u;
+    double D[9];
 #pragma unroll
-  for (int q = 0; q < 9; ++q) lam[q] = fmax(ds[q * kHessThreads], 0.0);
-  for (int i = 0; i < 9; ++i)
-    for (int j = 0; j <= i; ++j) {
-      double acc = 0.0;
+    for (int i = 0; i < 9; ++i) D[i] = __ldg(dminv + 9 * (size_t)e + i);
+    int4 t = __ldg(tets + e);
+    double x0[3], x1[3], x2[3], x3[3];
 #pragma unroll
-      for (int q = 0; q < 9; ++q) acc += Vs[(9 * i + q) * kHessThreads] * lam[q] * Vs[(9 * j + q) * kHessThreads];
-      o[JGS2_PK(i, j)] = acc;
+    for (int c = 0; c < 3; ++c) {
+      x0[c] = __ldg(xs + 3 * t.x + c); x1[c] = __ldg(xs + 3 * t.y + c);
+      x2[c] = __ldg(xs + 3 * t.z + c); x3[c] = __ldg(xs + 3 * t.w + c);
     }
+    double F[9];
+    deformation_gradient(x0, x1, x2, x3, D, F);
+    double4 ep = eprops[e];
+    double Mp[45];
+    reduced_hessian_closed(F, D, ep.x, snh_const(ep.y, ep.z), Mp);
+    double* o = mplus + 45 * (size_t)u;
+    if (is_pos_def9(Mp)) {
+#pragma unroll
+      for (int i = 0; i < 45; ++i) o[i] = Mp[i];
+    } else {
+      indef = true;
+      double* Vs = hsm + threadIdx.x;
+      double* ds = hsm + 81 * kHessThreads + threadIdx.x;
+      double* es = hsm + 90 * kHessThreads + threadIdx.x;
+#pragma unroll
+      for (int i = 0; i < 9; ++i)
+#pragma unroll
+        for (int j = 0; j <= i; ++j) {
+          Vs[(9 * i + j) * kHessThreads] = Mp[JGS2_PK(i, j)];
+          Vs[(9 * j + i) * kHessThreads] = Mp[JGS2_PK(i, j)];
+        }
+      sym_eig9_shared<kHessThreads>(Vs, ds, es);
+      double lam[9];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) lam[q] = fmax(ds[q * kHessThreads], 0.0);
+      for (int i = 0; i < 9; ++i)
+        for (int j = 0; j <= i; ++j) {
+          double acc = 0.0;
+#pragma unroll
+          for (int q = 0; q < 9; ++q)
+            acc += Vs[(9 * i + q) * kHessThreads] * lam[q] * Vs[(9 * j + q) * kHessThreads];
+          o[JGS2_PK(i, j)] = acc;
+        }
+    }
+  }
+  unsigned ball = __ballot_sync(0xffffffffu, indef);
+  if ((threadIdx.x & 31) == 0 && ball) atomicAdd(count, __popc(ball));
 }
 constexpr size_t kHessSmemBytes = 99 * kHessThreads * sizeof(double);
 
-// count: device int (zeroed here); list: device int[n] scratch.
+// count: device int, zeroed here; list: unused (kept for the call sites).
 inline void launch_element_mplus(int n, const int* elems, const double* xs, const int4* tets,
                                  const double* dminv, const double4* eprops, double* out, int* count,
-                                 int* list, cudaStream_t stream) {
+                                 int* /*list*/, cudaStream_t stream) {
   if (n <= 0) return;
   int grid = (n + kHessThreads - 1) / kHessThreads;
   cudaMemsetAsync(count, 0, sizeof(int), stream);
-  k_hess_pass1<<<grid, kHessThreads, 0, stream>>>(n, elems, xs, tets, dminv, eprops, out, count, list);
-  k_hess_pass2<<<grid, kHessThreads, kHessSmemBytes, stream>>>(count, list, out);
+  k_element_mplus<<<grid, kHessThreads, kHessSmemBytes, stream>>>(n, elems, xs, tets, dminv, eprops, out,
+                                                                  count);
 }
 
 }  // namespace jgs2

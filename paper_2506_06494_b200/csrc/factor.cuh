@@ -526,7 +526,7 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
     JGS2_CUDA(cudaMallocAsync(&tmp_list, (size_t)std::max(ne, 1) * sizeof(int), C.stream));
     launch_element_mplus(ne, nullptr, C.rest, C.tets, C.dminv, C.eprops, mp_all, C.hess_count, tmp_list,
                          C.stream);
-    C.launches += 2;
+    C.launches += 1;
     JGS2_CUDA(cudaFreeAsync(tmp_list, C.stream));
     C.check_launch();
   }

@@ -25,6 +25,8 @@ jgs2::Ctx::~Ctx() {
   if (cublas) cublasDestroy(cublas);
   if (cusolver) cusolverDnDestroy(cusolver);
   if (stream2) cudaStreamSynchronize(stream2);
+  tri_grid_free(pair_grid);
+  tri_grid_free(cap_grid);
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
   if (stream2) cudaStreamDestroy(stream2);
@@ -155,12 +157,12 @@ void hessians_async(Ctx& C) {
   }
   launch_element_mplus(C.nuniq, C.uniq, C.x, C.tets, C.dminv, C.eprops, C.mplus, C.hess_count,
                        C.hess_list, C.stream2);
-  C.launches += 2;
+  C.launches += 1;
   C.check_launch();
   if (C.profiling) {
     cudaEvent_t b = C.take_event();
     JGS2_CUDA(cudaEventRecord(b, C.stream2));
-    C.phase_launch[3] += 2;
+    C.phase_launch[3] += 1;
     C.pending.push_back({3, {a, b}});
   }
   JGS2_CUDA(cudaEventRecord(C.ev_join, C.stream2));
@@ -314,7 +316,7 @@ jgs2_ctx* jgs2_create(int32_t device) {
     JGS2_CUDA(cudaStreamCreateWithFlags(&C.stream2, cudaStreamNonBlocking));
     JGS2_CUDA(cudaEventCreateWithFlags(&C.ev_fork, cudaEventDisableTiming));
     JGS2_CUDA(cudaEventCreateWithFlags(&C.ev_join, cudaEventDisableTiming));
-    cudaFuncSetAttribute(k_hess_pass2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_element_mplus, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kHessSmemBytes);
 
   } catch (...) {
@@ -491,20 +493,21 @@ int32_t jgs2_set_precompute(jgs2_ctx* ctx, const jgs2_precompute* p, const jgs2_
     C.ls_cnt = C.alloc<int>(C.max_halvings + 2);
     C.ls_final = C.alloc<int>(4);
     JGS2_CUDA(cudaMemsetAsync(C.ls_final, 0, 4 * sizeof(int), C.stream));
-    // retained rows CSR (contact coupling rows)
-    std::vector<int> vptr(nv + 1, 0), vkeys;
-    std::vector<double> vrows;
-    for (int v = 0; v < nv; ++v) {
-      int k = bidx[v];
-      if (k >= 0) {
-        for (int64_t q = p->vrows_ptr[k]; q < p->vrows_ptr[k + 1]; ++q) {
-          vkeys.push_back((int)p->vrows_keys[q]);
-          vrows.insert(vrows.end(), p->vrows + 9 * q, p->vrows + 9 * q + 9);
-        }
-      }
-      vptr[v + 1] = (int)vkeys.size();
-    }
+    // retained rows CSR (contact coupling rows, local_solver.py:85-112): only
+    // surface vertices can be pair members, so only their bases are kept.
     if (contact_active(C)) {
+      std::vector<int> vptr(nv + 1, 0), vkeys;
+      std::vector<double> vrows;
+      for (int v = 0; v < nv; ++v) {
+        int k = bidx[v];
+        if (k >= 0 && C.h_surface[v]) {
+          for (int64_t q = p->vrows_ptr[k]; q < p->vrows_ptr[k + 1]; ++q) {
+            vkeys.push_back((int)p->vrows_keys[q]);
+            vrows.insert(vrows.end(), p->vrows + 9 * q, p->vrows + 9 * q + 9);
+          }
+        }
+        vptr[v + 1] = (int)vkeys.size();
+      }
       C.vr_ptr = C.upload(vptr.data(), vptr.size());
       C.vr_keys = C.upload(vkeys.data(), vkeys.size());
       C.vr_rows = C.upload(vrows.data(), vrows.size());

@@ -86,73 +86,65 @@ class Precompute:
           of the identity at incident/cubature vertices (the shape of a true
           perturbation basis, which decays away from the vertex).
         """
+        import scipy.sparse as sp
         rng = np.random.default_rng(seed)
         nv, ne = model.num_vertices, model.num_elements
-        tets = np.asarray(model.tets)
+        tets = np.asarray(model.tets, dtype=np.int64)
         free = np.flatnonzero(~np.asarray(model.fixed_mask))
-        diag = rest_diagonal_blocks(model, h_ref)
+        nf = free.size
+        diag = rest_diagonal_blocks_chunked(model, h_ref)
+        flat = tets.ravel()
+        eid = np.repeat(np.arange(ne, dtype=np.int64), 4)
         ptr_inc = np.zeros(nv + 1, dtype=np.int64)
-        np.cumsum(np.bincount(tets.ravel(), minlength=nv), out=ptr_inc[1:])
-        inc = np.argsort(tets.ravel(), kind="stable") // 4
+        np.cumsum(np.bincount(flat, minlength=nv), out=ptr_inc[1:])
+        inc = eid[np.argsort(flat, kind="stable")]
         tb = np.asarray(getattr(model, "tet_body", np.zeros(ne, dtype=np.int64)))
-        body_lo = np.zeros(ne, dtype=np.int64)
-        body_hi = np.zeros(ne, dtype=np.int64)
-        for b in np.unique(tb):
-            idx = np.flatnonzero(tb == b)
-            body_lo[idx] = idx.min()
-            body_hi[idx] = idx.max() + 1
-        # Cubature samples: element ids near an incident element, rejecting
-        # incident ones (retry by shifting).
-        first_inc = inc[ptr_inc[free]]
-        off = rng.integers(24, 4000, size=(free.size, samples)) * \
-            rng.choice((-1, 1), size=(free.size, samples))
-        cand = first_inc[:, None] + off
+        starts = np.flatnonzero(np.r_[True, tb[1:] != tb[:-1]])
+        ends = np.r_[starts[1:], ne]
+        seg = np.searchsorted(starts, np.arange(ne), side="right") - 1
+        body_lo, body_hi = starts[seg], ends[seg]
+        has_inc = ptr_inc[free + 1] > ptr_inc[free]
+        first_inc = np.where(has_inc, inc[np.minimum(ptr_inc[free], max(inc.size - 1, 0))], 0)
+        # cubature samples: element ids at random offsets from an incident
+        # element (same body), sorted, de-duplicated, never incident
+        off = rng.integers(24, 4000, size=(nf, samples)) * rng.choice((-1, 1), size=(nf, samples))
         lo = body_lo[first_inc][:, None]
-        hi = body_hi[first_inc][:, None]
-        span = np.maximum(hi - lo, 1)
-        cand = lo + np.mod(cand - lo, span)
-        cub = np.sort(cand, axis=1)
-        # drop duplicates / incident collisions by nudging (rare)
-        for c in range(1, samples):
-            dup = cub[:, c] <= cub[:, c - 1]
-            cub[dup, c] = np.minimum(cub[dup, c - 1] + 1, hi[dup, 0] - 1)
-        inc_sets = [set(inc[ptr_inc[v]:ptr_inc[v + 1]].tolist()) for v in free] \
-            if free.size <= 200000 else None
+        span = np.maximum(body_hi[first_inc][:, None] - lo, 1)
+        cub = np.sort(lo + np.mod(first_inc[:, None] + off - lo, span), axis=1)
+        dup = np.zeros_like(cub, dtype=bool)
+        dup[:, 1:] = cub[:, 1:] == cub[:, :-1]
+        inc_key = np.sort(flat * ne + eid) if ne else np.zeros(0, np.int64)
+        q = free[:, None] * ne + cub
+        pos = np.searchsorted(inc_key, q)
+        is_inc = (pos < inc_key.size) & (inc_key[np.minimum(pos, inc_key.size - 1)] == q)
+        valid = ~(dup | is_inc | ~has_inc[:, None])
         weights = weight_scale * rng.uniform(0.5, 1.5, size=cub.shape)
-        # Retained rows: own, incident-element vertices, cubature vertices.
+        # retained rows: own + incident-element vertices + cubature corners
+        A = sp.csr_matrix((np.ones(flat.size, dtype=np.int8), (flat, eid)), shape=(nv, max(ne, 1)))
+        adj = (A @ A.T)[free]
+        rows_c = np.repeat(np.arange(nf), 4 * samples)
+        cols_c = tets[np.where(valid, cub, 0)].reshape(nf, -1)
+        keep_c = np.repeat(valid, 4, axis=1).ravel()
+        Pc = sp.csr_matrix((np.ones(int(keep_c.sum()), dtype=np.int8),
+                            (rows_c[keep_c], cols_c.ravel()[keep_c])), shape=(nf, nv))
+        I = sp.csr_matrix((np.ones(nf, dtype=np.int8), (np.arange(nf), free)), shape=(nf, nv))
+        K = (adj.astype(bool) + Pc.astype(bool) + I.astype(bool)).tocsr()
+        K.sort_indices()
+        keys = K.indices.astype(np.int64)
+        ptr = K.indptr.astype(np.int64)
+        owner = np.repeat(free, np.diff(ptr))
         x0 = np.asarray(model.rest_positions)
         ext = float(np.ptp(x0, axis=0).max()) or 1.0
-        keys_list, ptr = [], [0]
-        for k, v in enumerate(free):
-            kk = set(tets[inc[ptr_inc[v]:ptr_inc[v + 1]]].ravel().tolist())
-            kk.add(int(v))
-            elems = cub[k]
-            if inc_sets is not None:
-                bad = [e for e in elems if e in inc_sets[k]]
-                if bad:
-                    keep = [e for e in elems if e not in inc_sets[k]]
-                    elems = np.array(keep, dtype=np.int64)
-                    weights_k = weights[k][:len(keep)]
-                    cub[k, :len(keep)] = elems
-                    cub[k, len(keep):] = -1
-                    weights[k, :len(keep)] = weights_k
-                    weights[k, len(keep):] = 0.0
-            kk.update(tets[elems[elems >= 0]].ravel().tolist())
-            keys_list.append(np.array(sorted(kk), dtype=np.int64))
-            ptr.append(ptr[-1] + len(kk))
-        keys = np.concatenate(keys_list) if keys_list else np.zeros(0, np.int64)
-        owner = np.repeat(free, np.diff(ptr))
         dist = np.linalg.norm(x0[keys] - x0[owner], axis=1) / ext
         scale = np.where(keys == owner, 1.0, 0.6 * np.exp(-8.0 * dist))
-        vrows = scale[:, None, None] * np.eye(3)[None]
-        valid = cub >= 0
-        cptr = np.zeros(free.size + 1, dtype=np.int64)
+        vrows = np.zeros((keys.size, 3, 3))
+        vrows[:, 0, 0] = vrows[:, 1, 1] = vrows[:, 2, 2] = scale
+        cptr = np.zeros(nf + 1, dtype=np.int64)
         np.cumsum(valid.sum(axis=1), out=cptr[1:])
         return cls(vertices=free.astype(np.int64), gbar=-diag[free],
                    group=free[:, None].astype(np.int64), gbar_rows=-diag[free],
-                   vrows_ptr=np.array(ptr, dtype=np.int64), vrows_keys=keys,
-                   vrows=vrows, cub_ptr=cptr, cub_elems=cub[valid].astype(np.int64),
-                   cub_weights=weights[valid])
+                   vrows_ptr=ptr, vrows_keys=keys, vrows=vrows, cub_ptr=cptr,
+                   cub_elems=cub[valid].astype(np.int64), cub_weights=weights[valid])
 
 
 def rest_diagonal_blocks(model, h_ref):
@@ -199,4 +191,22 @@ def rest_diagonal_blocks(model, h_ref):
     for m in range(4):
         blk = np.einsum("ej,ejrks,ek->ers", W[:, m], H9b, W[:, m]) * vol[:, None, None]
         np.add.at(out, tets[:, m], blk)
+    return out
+
+
+def rest_diagonal_blocks_chunked(model, h_ref, chunk=400000):
+    """rest_diagonal_blocks over element chunks (bounded temporaries)."""
+    class _View:
+        pass
+    ne = model.num_elements
+    out = None
+    for a in range(0, max(ne, 1), chunk):
+        v = _View()
+        sl = slice(a, min(ne, a + chunk))
+        v.tets, v.mu, v.lam = np.asarray(model.tets)[sl], np.asarray(model.mu)[sl], np.asarray(model.lam)[sl]
+        v.dm_inv, v.volumes = np.asarray(model.dm_inv)[sl], np.asarray(model.volumes)[sl]
+        v.num_vertices = model.num_vertices
+        v.masses = np.asarray(model.masses) if a == 0 else np.zeros(model.num_vertices)
+        blk = rest_diagonal_blocks(v, h_ref)
+        out = blk if out is None else out + blk
     return out

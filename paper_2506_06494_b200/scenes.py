@@ -77,32 +77,46 @@ def puffer_ball_mesh(radius=0.5, cells=40, spikes=12, spike_amp=0.25, seed=0, ce
     return build_mesh(verts, tets)
 
 
-def puffer_balls(n_balls=1, cells=40, young=2e7, soft_young=None, plane_only=True, gap=0.15):
-    """C2 (n_balls=1, ground plane) / C4 (10 balls, glass tank) scene."""
-    bodies = []
-    meshes = []
-    r = 0.5
-    for b in range(n_balls):
-        m = puffer_ball_mesh(radius=r, cells=cells, seed=b)
-        meshes.append(m)
-    ext = 2 * r * 1.25
-    per_row = max(1, int(np.ceil(np.sqrt(n_balls))))
-    for b, m in enumerate(meshes):
-        e = young if (soft_young is None or b % 2 == 0) else soft_young
-        mat = MaterialParams.from_young_poisson(e, 0.4, 1000.0)
-        ix, iz = b % per_row, (b // per_row) % per_row
-        iy = b // (per_row * per_row)
-        t = np.array([ix * (ext + gap), ext / 2 + 0.05 + iy * (ext + gap), iz * (ext + gap)])
-        bodies.append((m, mat, np.zeros(0, dtype=np.int64), t, np.eye(3)))
+def puffer_balls(n_balls=1, cells=45, youngs=(2e7,), ncols=4, gap=0.2, walls=False, radius=0.5):
+    """C2 (1 ball on the ground plane) / C4 (10 balls in a glass tank).
+
+    Balls stand in columns (ncols per layer, 2 x 2 footprint); the lowest
+    vertex of a bottom ball and of every stacked ball sits 0.5 dhat above
+    the ground / directly above the top vertex of the ball below, so the
+    barrier is active from the first sweep (plane and cross-body
+    vertex-triangle pairs). Tank walls (C4) are 0.5 dhat outside the
+    outermost vertices. dhat = 1% of the ball extent, kappa = 2e3
+    (cube_drop.toml:18-24). Materials cycle through ``youngs``.
+    """
+    meshes = [puffer_ball_mesh(radius=radius, cells=cells, seed=b) for b in range(n_balls)]
+    ext = 2.0 * radius * 1.25
     dhat = 0.01 * ext
+    spacing = ext + gap
+    bodies, world = [], []
+    tops = {}
+    for b, m in enumerate(meshes):
+        col, layer = b % ncols, b // ncols
+        base = np.array([(col % 2) * spacing, 0.0, (col // 2) * spacing])
+        x = m.rest_positions
+        lo = int(np.argmin(x[:, 1]))
+        if layer == 0:
+            t = base - np.array([0.0, x[lo, 1], 0.0]) + np.array([0.0, 0.5 * dhat, 0.0])
+        else:
+            top = tops[col]
+            t = top - x[lo] + np.array([0.0, 0.5 * dhat, 0.0])
+        xw = x + t
+        tops[col] = xw[int(np.argmax(xw[:, 1]))]
+        world.append(xw)
+        mat = MaterialParams.from_young_poisson(youngs[b % len(youngs)], 0.4, 1000.0)
+        bodies.append((m, mat, np.zeros(0, dtype=np.int64), t, np.eye(3)))
     planes = [HalfSpace(np.zeros(3), np.array([0.0, 1.0, 0.0]))]
-    if not plane_only:
-        lo = -ext / 2 - gap
-        hi = (per_row - 1) * (ext + gap) + ext / 2 + gap
-        planes += [HalfSpace(np.array([lo, 0, 0]), np.array([1.0, 0, 0])),
-                   HalfSpace(np.array([hi, 0, 0]), np.array([-1.0, 0, 0])),
-                   HalfSpace(np.array([0, 0, lo]), np.array([0, 0, 1.0])),
-                   HalfSpace(np.array([0, 0, hi]), np.array([0, 0, -1.0]))]
+    if walls:
+        allx = np.vstack(world)
+        lo, hi = allx.min(axis=0) - 0.5 * dhat, allx.max(axis=0) + 0.5 * dhat
+        planes += [HalfSpace(np.array([lo[0], 0, 0]), np.array([1.0, 0, 0])),
+                   HalfSpace(np.array([hi[0], 0, 0]), np.array([-1.0, 0, 0])),
+                   HalfSpace(np.array([0, 0, lo[2]]), np.array([0, 0, 1.0])),
+                   HalfSpace(np.array([0, 0, hi[2]]), np.array([0, 0, -1.0]))]
     return Model(bodies, planes=planes, barrier=BarrierParams(dhat=dhat, kappa=2e3))
 
 
@@ -123,6 +137,18 @@ def build(name):
         m = cantilever(divisions=(160, 40, 26), extents=(8.0, 2.0, 1.3), young=2e7)
         return m, predictor_state(m, twist_state(m)), H, \
             "C3 stiff beam twist box_grid(160,40,26) 998,400 tets, E=2e7, no contact"
+    if name == "c2":
+        m = puffer_balls(1, cells=45, youngs=(2e7,))
+        return m, predictor_state(m, SystemState.initial(m, H)), H, \
+            f"C2 puffer ball {m.num_elements:,} tets on a ground plane, E=2e7, IPC barrier"
+    if name == "c4":
+        m = puffer_balls(10, cells=45, youngs=(1e6, 5e4), walls=True)
+        return m, predictor_state(m, SystemState.initial(m, H)), H, \
+            f"C4 ten puffer balls {m.num_elements:,} tets in a 5-plane tank, E 1e6/5e4, IPC"
+    if name.startswith("c4s"):  # scaled-down C4 (tests / CPU samples): c4s<cells>
+        cells = int(name[3:] or 12)
+        m = puffer_balls(10, cells=cells, youngs=(1e6, 5e4), walls=True)
+        return m, predictor_state(m, SystemState.initial(m, H)), H, f"C4 at {cells} cells/ball"
     if name.startswith("c3s"):  # scaled-down C3 for tests / CPU samples: c3s<k>
         k = int(name[3:] or 4)
         m = cantilever(divisions=(160 // k, 40 // k, max(26 // k, 2)),
