@@ -121,11 +121,42 @@ void build_symbolic(int n, const int64_t* adj_ptr, const int32_t* adj, const dou
   b.side.assign(n, -1);
   b.order.reserve(n);
   b.S = &S;
-  std::vector<int> v(n);
-  std::iota(v.begin(), v.end(), 0);
-  // Disconnected components are handled by the bisection itself (empty
-  // separators become zero-column joining fronts).
-  b.dissect(v, 0, n, 0);
+  // Connected components first: each is dissected on its own coordinates
+  // (bodies of a multi-body scene share overlapping rest frames, so a
+  // geometric split across components would be meaningless), and the
+  // component roots are joined pairwise by zero-column fronts.
+  std::vector<int> comp(n, -1), v;
+  v.reserve(n);
+  std::vector<int> cstart;
+  for (int s = 0; s < n; ++s) {
+    if (comp[s] >= 0) continue;
+    int c = (int)cstart.size();
+    cstart.push_back((int)v.size());
+    comp[s] = c;
+    size_t head = v.size();
+    v.push_back(s);
+    while (head < v.size()) {
+      int u = v[head++];
+      for (int64_t e = adj_ptr[u]; e < adj_ptr[u + 1]; ++e) {
+        int w = adj[e];
+        if (comp[w] < 0) { comp[w] = c; v.push_back(w); }
+      }
+    }
+  }
+  cstart.push_back(n);
+  std::vector<int> roots;
+  for (size_t c = 0; c + 1 < cstart.size(); ++c) roots.push_back(b.dissect(v, cstart[c], cstart[c + 1], 0));
+  while (roots.size() > 1) {
+    std::vector<int> next;
+    for (size_t k = 0; k + 1 < roots.size(); k += 2) {
+      int id = b.new_front(nullptr, 0);
+      S.parent[roots[k]] = id; b.kids[id].push_back(roots[k]);
+      S.parent[roots[k + 1]] = id; b.kids[id].push_back(roots[k + 1]);
+      next.push_back(id);
+    }
+    if (roots.size() % 2) next.push_back(roots.back());
+    roots.swap(next);
+  }
   if ((int)b.order.size() != n) throw std::runtime_error("nested dissection lost vertices");
   S.perm = b.order;
   S.iperm.assign(n, -1);
