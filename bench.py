@@ -151,7 +151,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--config", default=os.environ.get("JGS2_BENCH_CONFIG", "c3"))
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     world, rank, local, dist = dist_setup()
@@ -191,19 +191,20 @@ def main():
     cfg = SolverConfig(max_outer=500)
     solver = LocalSolver(m, cfg, precompute=pre, h_ref=h, device=local if world > 1 else 0)
     fi = solver.factor_info
-    x_start = st.x.copy()
-    solver.set_state(st.x, st.z, h)
-    for _ in range(args.warmup):
-        solver.sweep_resident(True)
-    solver.set_state(x_start, st.z, h)
+    from paper_2506_06494_b200.model import SystemState
+    init = SystemState(x=st.x_prev.copy(), x_prev=st.x_prev.copy(), v=st.v.copy(), z=st.z.copy(), h=h)
+    # the simulation runs on the device: timesteps (compute_z, capped
+    # initialize_step, sweeps to tol_dx, velocity update) continue across
+    # the warm-up and timed windows; a step is one sweep.
+    solver.set_frame_state(init, m.gravity)
+    solver.run_sweeps(args.warmup)
     solver.phase_reset()
     solver.profile(True)
     launches0 = solver.kernel_launches
     barrier(dist)
     clocks = Clocks(local)
     solver.timer_start()
-    for _ in range(args.steps):
-        solver.sweep_resident(True)
+    frames_done = solver.run_sweeps(args.steps)
     ms = solver.timer_stop()
     clk = clocks.stop()
     launches = solver.kernel_launches - launches0
@@ -219,31 +220,42 @@ def main():
     achieved = d_bytes / (d_ms / 1e3) / 1e9 if d_ms > 0 else 0.0
     total_bytes = sum(p[2] for p in phases.values())
 
-    # end-to-end through the C ABI with pinned host buffers (x, z in; x, dx out)
+    # one full timestep to the residual tolerance, device-resident
+    solver.timer_start()
+    (ts_iters, ts_conv), = solver.run_frames(1)
+    ts_ms = solver.timer_stop()
+
+    # end-to-end through the reference-facing API with host buffers: per
+    # frame compute_z (host), capped initialize_step, sweeps through the
+    # C-ABI host call (x, z pinned in; x, dx out every sweep), velocity update
     nv = m.num_vertices
     xin, o1 = L.pinned_array((nv, 3))
     zin, o2 = L.pinned_array((nv, 3))
     xout, o3 = L.pinned_array((nv, 3))
     dxo, o4 = L.pinned_array((nv, 3))
-    xin[:] = x_start
-    zin[:] = st.z
+    xp, vv = solver.get_frame_state()
+    hs = SystemState(x=xp.copy(), x_prev=xp.copy(), v=vv.copy(), z=xp.copy(), h=h)
     inf = L.SweepInfo()
     import ctypes
-    solver.timer_start()
-    for _ in range(args.e2e_steps):
-        L.check(solver._lib.jgs2_sweep_host(solver._ctx, L.ptr(xin, L.f64), L.ptr(zin, L.f64), h,
-                                            None, L.ptr(xout, L.f64), L.ptr(dxo, L.f64),
-                                            ctypes.byref(inf)), solver._ctx)
-        xin[:] = xout
-    e2e_ms = max_over_ranks(dist, solver.timer_stop())
-    e2e = world * args.e2e_steps / (e2e_ms / 1e3)
-
-    # one full timestep to the residual tolerance from the predictor
-    from paper_2506_06494_b200.model import SystemState
-    ts = SystemState(x=x_start.copy(), x_prev=st.x_prev.copy(), v=st.v.copy(), z=st.z.copy(), h=h)
-    solver.timer_start()
-    stats = solver.outer_solve(ts)
-    ts_ms = solver.timer_stop()
+    from paper_2506_06494_b200.model import compute_z, step_velocity_update
+    e2e_sweeps = 0
+    t_e2e = time.perf_counter()
+    while e2e_sweeps < args.e2e_steps:
+        compute_z(m, hs)
+        solver.initialize_step(hs)
+        xin[:] = hs.x
+        zin[:] = hs.z
+        for _ in range(cfg.max_outer):
+            L.check(solver._lib.jgs2_sweep_host(solver._ctx, L.ptr(xin, L.f64), L.ptr(zin, L.f64), h,
+                                                None, L.ptr(xout, L.f64), L.ptr(dxo, L.f64),
+                                                ctypes.byref(inf)), solver._ctx)
+            e2e_sweeps += 1
+            xin[:] = xout
+            if inf.dx_norm < cfg.tol_dx or e2e_sweeps >= args.e2e_steps:
+                break
+        step_velocity_update(m, hs, xin.copy())
+    e2e_s = max_over_ranks(dist, time.perf_counter() - t_e2e)
+    e2e = world * e2e_sweeps / e2e_s
 
     cpu = None
     if rank == 0 and not args.no_cpu:
@@ -268,8 +280,11 @@ def main():
                    "precompute": "injected (structurally valid; Precompute.injected)",
                    "cubature_samples": 6, "h": h, "parallelism": f"replicas x{world}",
                    "l2": "inputs > L2 (factor %.2f GB)" % (8 * fi.nnz_dof / 1e9)},
-        "timestep": {"iterations": stats.outer_iterations, "converged": stats.converged,
-                     "ms": ts_ms},
+        "timestep": {"iterations": ts_iters, "converged": ts_conv, "ms": ts_ms,
+                     "frames_in_window": len(frames_done),
+                     "mean_sweeps_per_frame": (float(np.mean(frames_done)) if frames_done else None),
+                     "ms_per_timestep": (ms / args.steps * float(np.mean(frames_done))
+                                         if frames_done else None)},
         "factor": {"nnz_L": int(fi.nnz_dof), "fronts": int(fi.nfronts), "levels": int(fi.nlevels),
                    "max_front": int(fi.max_front), "ordering": "geometric nested dissection",
                    "factor_s": round(solver.factor_seconds, 2), "precompute_s": round(t_pre, 2)},
@@ -280,7 +295,8 @@ def main():
                      "step_frac": (total_bytes / (ms / 1e3) / 1e9) / peak},
         "phases_ms_per_step": {p: round(v[0] / args.steps, 4) for p, v in phases.items()},
         "e2e": {"value": e2e, "unit": "sweeps/s", "h2d_bytes_per_step": 2 * 24 * nv,
-                "d2h_bytes_per_step": 2 * 24 * nv},
+                "d2h_bytes_per_step": 2 * 24 * nv, "sweeps": e2e_sweeps,
+                "timing": "wall clock incl. host frame driver (compute_z, velocity update)"},
         "gpu_launches": launches,
         "clocks": clk,
         "cpu_baseline": cpu,

@@ -157,6 +157,17 @@ int32_t jgs2_outer_solve(jgs2_ctx* ctx, double* dx_norms, double* grad_norms, do
                          double* max_local_steps, int64_t* activations, int32_t* iterations,
                          int32_t* converged);
 
+/* ---- frame driver (device-resident timesteps) ------------------------- */
+/* x_prev, v host arrays (nv*3), gravity[3]. */
+int32_t jgs2_set_frame_state(jgs2_ctx* ctx, const double* x_prev, const double* v, double h,
+                             const double* gravity);
+/* z = x_prev + h v + h^2 g (fixed: z = x_prev), x = x_prev + cap (z - x_prev)
+ * with cap = feasibility_step_cap (assembly.py:165-180, harness.py:130-134). */
+int32_t jgs2_frame_begin(jgs2_ctx* ctx, double* cap);
+/* v = (x - x_prev) / h; x_prev = x (assembly.py:346-351). */
+int32_t jgs2_frame_end(jgs2_ctx* ctx);
+int32_t jgs2_get_frame_state(jgs2_ctx* ctx, double* x_prev, double* v);
+
 /* ---- per-kernel entry points (parity tests; device state in/out) ------- */
 int32_t jgs2_total_energy(jgs2_ctx* ctx, const double* x, double* energy);
 int32_t jgs2_assembled_field(jgs2_ctx* ctx, double* g_asm /* nv*3 */);

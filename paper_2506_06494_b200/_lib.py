@@ -24,6 +24,7 @@ EXPORTS = (
     "jgs2_last_kernel_launches", "jgs2_sym_build", "jgs2_sym_sizes", "jgs2_sym_export",
     "jgs2_sym_free", "jgs2_profile", "jgs2_phase_stats", "jgs2_phase_reset", "jgs2_timer_start",
     "jgs2_timer_stop", "jgs2_pinned_alloc", "jgs2_pinned_free", "jgs2_step_cap",
+    "jgs2_set_frame_state", "jgs2_frame_begin", "jgs2_frame_end", "jgs2_get_frame_state",
 )
 PHASES = ("vertex_pass", "collect_rhs", "factor_solve", "cubature_hessians", "local_systems",
           "energy", "update", "contact")
@@ -132,6 +133,10 @@ def lib():
         "jgs2_pinned_alloc": (vp, [i64]),
         "jgs2_pinned_free": (None, [vp]),
         "jgs2_step_cap": (i32, [vp, P(f64), P(f64), P(f64)]),
+        "jgs2_set_frame_state": (i32, [vp, P(f64), P(f64), f64, P(f64)]),
+        "jgs2_frame_begin": (i32, [vp, P(f64)]),
+        "jgs2_frame_end": (i32, [vp]),
+        "jgs2_get_frame_state": (i32, [vp, P(f64), P(f64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

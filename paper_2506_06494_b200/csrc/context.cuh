@@ -160,6 +160,10 @@ struct Ctx {
   double* alpha0 = nullptr;    // nv
   int* kacc = nullptr;         // nv accept iteration of the local search
   double* dx = nullptr;        // nv*3
+  double* xprev = nullptr;     // frame state (device frame driver)
+  double* vel = nullptr;
+  double* dz = nullptr;
+  double gravity[3] = {0.0, 0.0, 0.0};
   bool rot_valid = false;
 
   // reductions

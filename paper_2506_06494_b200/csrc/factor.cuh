@@ -681,10 +681,13 @@ void factor_solve_launches(Ctx& C) {
   for (int l = 0; l < F.nlevels; ++l) {
     int64_t na = F.asm_level_ptr[l + 1] - F.asm_level_ptr[l];
     int64_t o = F.asm_level_ptr[l];
+    int nt = F.fwd_level_ptr[l + 1] - F.fwd_level_ptr[l];
+    if (na == 0 && nt == 0) continue;  // level of zero-size joining fronts
+    if (na > 0)
     k_fwd_assemble_flat<<<grid_for(na), kBlock, 0, C.stream>>>(na, F.asm_dst + o, F.asm_b + o,
                                                                F.asm_cp + o, F.asm_src, C.b, F.u, F.w);
     C.check_launch();
-    int nt = F.fwd_level_ptr[l + 1] - F.fwd_level_ptr[l];
+    if (nt == 0) continue;
     int g = std::min(nt, 148 * kApplyCtasPerSm);
     k_fwd_apply<<<g, kSolveThreads, 0, C.stream>>>(F.fwd_tasks + F.fwd_level_ptr[l], nt, F.f_colbeg,
                                                    F.f_ns, F.f_nr, F.f_ld, F.f_loff, F.f_uoff,
@@ -696,6 +699,7 @@ void factor_solve_launches(Ctx& C) {
     if (nt == 0) continue;
     int64_t ng = F.gat_level_ptr[l + 1] - F.gat_level_ptr[l];
     int64_t o = F.gat_level_ptr[l];
+    if (ng > 0)
     k_bwd_gather_flat<<<grid_for(ng), kBlock, 0, C.stream>>>(ng, F.gat_dst + o, F.gat_src + o, C.b,
                                                              C.q, F.w);
     C.check_launch();
@@ -714,8 +718,15 @@ void factor_solve(Ctx& C) {
   if (!F.graph_exec) {
     int64_t l0 = C.launches;
     JGS2_CUDA(cudaStreamBeginCapture(C.stream, cudaStreamCaptureModeThreadLocal));
-    factor_solve_launches(C);
-    cudaGraph_t g;
+    cudaGraph_t g = nullptr;
+    try {
+      factor_solve_launches(C);
+    } catch (...) {
+      cudaStreamEndCapture(C.stream, &g);  // leave capture mode before reporting
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      throw;
+    }
     JGS2_CUDA(cudaStreamEndCapture(C.stream, &g));
     JGS2_CUDA(cudaGraphInstantiate(&F.graph_exec, g, 0));
     JGS2_CUDA(cudaGraphDestroy(g));

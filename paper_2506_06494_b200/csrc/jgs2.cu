@@ -673,6 +673,80 @@ int32_t jgs2_outer_solve(jgs2_ctx* ctx, double* dx_norms, double* grad_norms, do
   });
 }
 
+// ============================================================= frame driver
+// compute_z + initialize_step (assembly.py:165-180, harness.py:130-134) and
+// step_velocity_update (assembly.py:346-351) on device-resident state.
+namespace {
+__global__ void k_compute_z(int nv, const double* xp, const double* v, double h, double g0, double g1,
+                            double g2, const uint8_t* fixed, double* z, double* dz) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nv) return;
+  double g[3] = {g0, g1, g2};
+  for (int c = 0; c < 3; ++c) {
+    double zc = fixed[i] ? xp[3 * i + c] : (xp[3 * i + c] + h * v[3 * i + c]) + (h * h) * g[c];
+    z[3 * i + c] = zc;
+    dz[3 * i + c] = zc - xp[3 * i + c];
+  }
+}
+__global__ void k_init_x(int nv, const double* xp, const double* dz, double cap, double* x) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 3 * nv) return;
+  x[i] = xp[i] + cap * dz[i];
+}
+__global__ void k_velocity(int nv, double h, const double* x, double* xp, double* v) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 3 * nv) return;
+  v[i] = (x[i] - xp[i]) / h;
+  xp[i] = x[i];
+}
+}  // namespace
+
+int32_t jgs2_set_frame_state(jgs2_ctx* ctx, const double* x_prev, const double* v, double h,
+                             const double* gravity) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (!C.have_model) throw Error(JGS2_E_ARG, "model not set");
+    if (!(h > 0)) throw Error(JGS2_E_ARG, "h must be positive");
+    size_t n = 3 * (size_t)C.nv;
+    if (!C.xprev) { C.xprev = C.alloc<double>(n); C.vel = C.alloc<double>(n); C.dz = C.alloc<double>(n); }
+    JGS2_CUDA(cudaMemcpyAsync(C.xprev, x_prev, n * sizeof(double), cudaMemcpyHostToDevice, C.stream));
+    JGS2_CUDA(cudaMemcpyAsync(C.vel, v, n * sizeof(double), cudaMemcpyHostToDevice, C.stream));
+    for (int c = 0; c < 3; ++c) C.gravity[c] = gravity ? gravity[c] : 0.0;
+    C.h = h;
+    C.sync();
+  });
+}
+
+int32_t jgs2_frame_begin(jgs2_ctx* ctx, double* cap_out) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (!C.xprev) throw Error(JGS2_E_ARG, "frame state not set");
+    k_compute_z<<<grid_for(C.nv), kBlock, 0, C.stream>>>(C.nv, C.xprev, C.vel, C.h, C.gravity[0],
+                                                         C.gravity[1], C.gravity[2], C.fixed, C.z, C.dz);
+    C.check_launch();
+    double cap = contact_active(C) ? contact_step_cap(C, C.xprev, C.dz) : 1.0;
+    k_init_x<<<grid_for(3 * (int64_t)C.nv), kBlock, 0, C.stream>>>(C.nv, C.xprev, C.dz, cap, C.x);
+    C.check_launch();
+    C.sync();
+    if (cap_out) *cap_out = cap;
+  });
+}
+
+int32_t jgs2_frame_end(jgs2_ctx* ctx) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (!C.xprev) throw Error(JGS2_E_ARG, "frame state not set");
+    k_velocity<<<grid_for(3 * (int64_t)C.nv), kBlock, 0, C.stream>>>(C.nv, C.h, C.x, C.xprev, C.vel);
+    C.check_launch();
+  });
+}
+
+int32_t jgs2_get_frame_state(jgs2_ctx* ctx, double* x_prev, double* v) {
+  return guarded(ctx, [&](Ctx& C) {
+    size_t n = 3 * (size_t)C.nv * sizeof(double);
+    if (x_prev) JGS2_CUDA(cudaMemcpyAsync(x_prev, C.xprev, n, cudaMemcpyDeviceToHost, C.stream));
+    if (v) JGS2_CUDA(cudaMemcpyAsync(v, C.vel, n, cudaMemcpyDeviceToHost, C.stream));
+    C.sync();
+  });
+}
+
 // ============================================================= per-kernel entries
 int32_t jgs2_total_energy(jgs2_ctx* ctx, const double* x, double* energy) {
   return guarded(ctx, [&](Ctx& C) {

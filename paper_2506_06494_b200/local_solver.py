@@ -343,6 +343,59 @@ class LocalSolver:
         stats.wall_seconds = time.perf_counter() - t0
         return stats
 
+    # ------------------------------------------------- device frame driver
+    def set_frame_state(self, state, gravity):
+        """Upload (x_prev, v, h) for device-resident timesteps."""
+        g = L.f64a(gravity)
+        self._call(self._lib.jgs2_set_frame_state, L.ptr(L.f64a(state.x_prev), L.f64),
+                   L.ptr(L.f64a(state.v), L.f64), float(state.h), L.ptr(g, L.f64))
+
+    def run_frames(self, frames):
+        """``frames`` timesteps fully on the device: compute_z + capped
+        initialize_step, outer_solve sweeps to tol_dx, velocity update
+        (harness.py:187-211 without the file outputs). Returns per-frame
+        (iterations, converged)."""
+        out = []
+        cap = L.f64(1.0)
+        for _ in range(frames):
+            self._call(self._lib.jgs2_frame_begin, C_ref(cap))
+            it, conv = 0, False
+            for it in range(1, self.config.max_outer + 1):
+                info = self.sweep_resident(refresh_rotations=True)
+                if info["dx_norm"] < self.config.tol_dx:
+                    conv = True
+                    break
+            self._call(self._lib.jgs2_frame_end)
+            out.append((it, conv))
+        return out
+
+    def run_sweeps(self, budget):
+        """Continue the device-resident simulation for exactly ``budget``
+        sweeps (frames end on convergence; a frame still open when the
+        budget runs out is resumed by the next call). Returns the list of
+        iteration counts of the frames completed in this call."""
+        done = []
+        left = budget
+        cap = L.f64(1.0)
+        while left > 0:
+            if not getattr(self, "_frame_open", False):
+                self._call(self._lib.jgs2_frame_begin, C_ref(cap))
+                self._frame_open, self._frame_iters = True, 0
+            info = self.sweep_resident(refresh_rotations=True)
+            left -= 1
+            self._frame_iters += 1
+            if info["dx_norm"] < self.config.tol_dx or self._frame_iters >= self.config.max_outer:
+                self._call(self._lib.jgs2_frame_end)
+                done.append(self._frame_iters)
+                self._frame_open = False
+        return done
+
+    def get_frame_state(self):
+        xp = np.empty((self.nv, 3))
+        v = np.empty((self.nv, 3))
+        self._call(self._lib.jgs2_get_frame_state, L.ptr(xp, L.f64), L.ptr(v, L.f64))
+        return xp, v
+
     # ------------------------------------------------- per-kernel entry points
     def total_energy(self, x):
         e = L.f64(0.0)

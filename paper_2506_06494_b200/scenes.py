@@ -91,7 +91,8 @@ def puffer_balls(n_balls=1, cells=45, youngs=(2e7,), ncols=4, gap=0.2, walls=Fal
     meshes = [puffer_ball_mesh(radius=radius, cells=cells, seed=b) for b in range(n_balls)]
     ext = 2.0 * radius * 1.25
     dhat = 0.01 * ext
-    spacing = ext + gap
+    shift_max = 0.35 * radius  # horizontal alignment of a stacked ball, clamped
+    spacing = ext + gap + 2.0 * shift_max
     bodies, world = [], []
     tops = {}
     for b, m in enumerate(meshes):
@@ -102,10 +103,17 @@ def puffer_balls(n_balls=1, cells=45, youngs=(2e7,), ncols=4, gap=0.2, walls=Fal
         if layer == 0:
             t = base - np.array([0.0, x[lo, 1], 0.0]) + np.array([0.0, 0.5 * dhat, 0.0])
         else:
-            top = tops[col]
+            # lowest vertex 0.5 dhat above the top vertex of the ball below
+            # (the whole ball stays above that height: no overlap), shifted
+            # sideways to sit over it when that needs <= shift_max
+            top, cen = tops[col]
             t = top - x[lo] + np.array([0.0, 0.5 * dhat, 0.0])
+            off = t[[0, 2]] - cen[[0, 2]]
+            n_off = float(np.linalg.norm(off))
+            if n_off > shift_max:
+                t[[0, 2]] = cen[[0, 2]] + off * (shift_max / n_off)
         xw = x + t
-        tops[col] = xw[int(np.argmax(xw[:, 1]))]
+        tops[col] = (xw[int(np.argmax(xw[:, 1]))], base)
         world.append(xw)
         mat = MaterialParams.from_young_poisson(youngs[b % len(youngs)], 0.4, 1000.0)
         bodies.append((m, mat, np.zeros(0, dtype=np.int64), t, np.eye(3)))

@@ -141,3 +141,19 @@ def test_contact_sweeps_match_oracle():
         dxb, ib = o.sweep(b, orc.vertex_rotations(m, b.x))
         assert ia["line_search_activations"] == ib["line_search_activations"]
         assert rel_err(a.x, b.x) < 1e-9
+
+
+@pytest.mark.parametrize("name", ("beam", "two_body", "cube_drop"))
+def test_device_frame_driver_matches_reference(golden, name):
+    """compute_z + capped initialize_step + outer_solve + velocity update
+    fully on the device (harness.py:187-202) reproduce the reference
+    trajectory frame by frame."""
+    from paper_2506_06494_b200.model import SystemState
+    g = golden(name)
+    model, s, h = gpu_solver(g)
+    st = SystemState.initial(model, h)
+    s.set_frame_state(st, model.gravity)
+    for f in range(g["frame_iterations"].size):
+        (it, conv), = s.run_frames(1)
+        assert it == int(g["frame_iterations"][f]), (f, it)
+        assert rel_err(s.get_x(), g["frame_x_final"][f]) < 1e-9
