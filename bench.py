@@ -188,7 +188,7 @@ def main():
     t0 = time.perf_counter()
     pre = Precompute.injected(m, h, samples=6, seed=0)
     t_pre = time.perf_counter() - t0
-    cfg = SolverConfig(max_outer=500)
+    cfg = SolverConfig(max_outer=500, tol_dx=getattr(m, "tol_dx", 1e-3))
     solver = LocalSolver(m, cfg, precompute=pre, h_ref=h, device=local if world > 1 else 0)
     fi = solver.factor_info
     from paper_2506_06494_b200.model import SystemState
@@ -197,14 +197,15 @@ def main():
     # initialize_step, sweeps to tol_dx, velocity update) continue across
     # the warm-up and timed windows; a step is one sweep.
     solver.set_frame_state(init, m.gravity)
-    solver.run_sweeps(args.warmup)
+    episode = getattr(m, "episode_frames", None)
+    solver.run_sweeps(args.warmup, episode)
     solver.phase_reset()
     solver.profile(True)
     launches0 = solver.kernel_launches
     barrier(dist)
     clocks = Clocks(local)
     solver.timer_start()
-    frames_done = solver.run_sweeps(args.steps)
+    frames_done = solver.run_sweeps(args.steps, episode)
     ms = solver.timer_stop()
     clk = clocks.stop()
     launches = solver.kernel_launches - launches0
@@ -280,6 +281,7 @@ def main():
                    "precompute": "injected (structurally valid; Precompute.injected)",
                    "cubature_samples": 6, "h": h, "parallelism": f"replicas x{world}",
                    "l2": "inputs > L2 (factor %.2f GB)" % (8 * fi.nnz_dof / 1e9)},
+        "episode_frames": episode,
         "timestep": {"iterations": ts_iters, "converged": ts_conv, "ms": ts_ms,
                      "frames_in_window": len(frames_done),
                      "mean_sweeps_per_frame": (float(np.mean(frames_done)) if frames_done else None),

@@ -164,6 +164,8 @@ int32_t jgs2_set_frame_state(jgs2_ctx* ctx, const double* x_prev, const double* 
 /* z = x_prev + h v + h^2 g (fixed: z = x_prev), x = x_prev + cap (z - x_prev)
  * with cap = feasibility_step_cap (assembly.py:165-180, harness.py:130-134). */
 int32_t jgs2_frame_begin(jgs2_ctx* ctx, double* cap);
+/* restore the frame state saved by jgs2_set_frame_state (device copy) */
+int32_t jgs2_frame_reset(jgs2_ctx* ctx);
 /* v = (x - x_prev) / h; x_prev = x (assembly.py:346-351). */
 int32_t jgs2_frame_end(jgs2_ctx* ctx);
 int32_t jgs2_get_frame_state(jgs2_ctx* ctx, double* x_prev, double* v);

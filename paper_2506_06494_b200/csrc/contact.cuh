@@ -460,28 +460,66 @@ __global__ void k_sv_maxstep(ContactDev cd, const double* dx, double* partials, 
   grid_reduce<OP_MAX>(mx, partials, counter, out);
 }
 
-// min over cross-body (vertex, triangle) candidates of dist / rate
-__global__ void k_cap_tris(ContactDev cd, TriGridDev g, const double* x, const double* dx, double* partials,
-                           unsigned* counter, double* out) {
+// min over cross-body (vertex, triangle) pairs of dist / rate, rate =
+// |dx_v| + max corner |dx_t|. Only pairs with dist < rate / 0.9 can lower
+// the cap below 1; triangles are inflated by s_t / 0.9 and each vertex
+// scans the cells its box of half-size s_v / 0.9 overlaps (a pair with
+// dist < (s_v + s_t) / 0.9 always meets; repeats are harmless for a min).
+__global__ void k_cap_tris(ContactDev cd, TriGridDev g, const double* x, const double* dx, double vscale,
+                           double* partials, unsigned* counter, double* out) {
   double mn = INFINITY;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cd.nsv; i += gridDim.x * blockDim.x) {
     int v = cd.sv[i];
     double p[3] = {x[3 * v], x[3 * v + 1], x[3 * v + 2]};
     double sp = norm3_np(dx + 3 * v);
+    double rv = vscale * sp;
     int bv = cd.vbody[v];
-    long long q0, q1;
-    grid_range(g, point_key(p, g.inv_cell), &q0, &q1);
-    for (long long q = q0; q < q1; ++q) {
-      int t = g.tris[q];
-      if (cd.tbody[t] == bv) continue;
+    long long lo[3], hi[3];
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = cell_coord(p[k] - rv, g.inv_cell);
+      hi[k] = cell_coord(p[k] + rv, g.inv_cell);
+    }
+    auto visit = [&](int t) {
+      if (cd.tbody[t] == bv) return;
       int a0 = cd.st[3 * t], a1 = cd.st[3 * t + 1], a2 = cd.st[3 * t + 2];
-      double st = fmax(fmax(norm3_np(dx + 3 * a0), norm3_np(dx + 3 * a1)), norm3_np(dx + 3 * a2));
-      double rate = sp + st;
-      if (!(rate > 1e-30)) continue;
+      double stt = fmax(fmax(norm3_np(dx + 3 * a0), norm3_np(dx + 3 * a1)), norm3_np(dx + 3 * a2));
+      double rate = sp + stt;
+      if (!(rate > 1e-30)) return;
       double bary[3];
       double d = closest_point_tri(p, x + 3 * a0, x + 3 * a1, x + 3 * a2, bary);
       mn = fmin(mn, d / rate);
+    };
+    int no = *g.n_over;
+    for (int q = 0; q < no; ++q) visit(g.over[q]);
+    long long ncell = (hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1) * (hi[2] - lo[2] + 1);
+    if (!(ncell > 0 && ncell <= kMaxCellsPerTri)) {  // fast vertex: scan every triangle
+      for (int t = 0; t < cd.nst; ++t) visit(t);
+      continue;
     }
+    for (long long ci = lo[0]; ci <= hi[0]; ++ci)
+      for (long long cj = lo[1]; cj <= hi[1]; ++cj)
+        for (long long ck = lo[2]; ck <= hi[2]; ++ck) {
+          long long q0, q1;
+          grid_range(g, cell_key(ci, cj, ck), &q0, &q1);
+          for (long long q = q0; q < q1; ++q) visit(g.tris[q]);
+        }
+  }
+  grid_reduce<OP_MIN>(mn, partials, counter, out);
+}
+
+// min over the active triangle pairs of the current pair table of d / rate
+// (an upper bound source for the cap: these pairs are among all pairs)
+__global__ void k_cap_pairtable(int npairs, const double* rows, const double* dx, double* partials,
+                                unsigned* counter, double* out) {
+  double mn = INFINITY;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < npairs; k += gridDim.x * blockDim.x) {
+    const double* r = rows + (size_t)kPairRow * k;
+    if (r[0] == 0.0) continue;
+    double sp = norm3_np(dx + 3 * (int)r[1]);
+    double stt = fmax(fmax(norm3_np(dx + 3 * (int)r[2]), norm3_np(dx + 3 * (int)r[3])),
+                      norm3_np(dx + 3 * (int)r[4]));
+    double rate = sp + stt;
+    if (rate > 1e-30) mn = fmin(mn, r[6] / rate);
   }
   grid_reduce<OP_MIN>(mn, partials, counter, out);
 }
@@ -639,37 +677,44 @@ void contact_add_gradients(Ctx& C) {
   C.check_launch();
 }
 
-double contact_step_cap(Ctx& C, const double* x, const double* dx) {
+// feasibility_step_cap (assembly.py:263-291). pairs_at_x: the pair table
+// holds the pairs detected at this x (their d equal the reference's
+// closest-point distances bitwise) and gives an upper bound cap_ub; only
+// pairs with dist < cap_ub (s_v + s_t) / 0.9 can lower it further, so the
+// grid radii scale with cap_ub (exact).
+double contact_step_cap(Ctx& C, const double* x, const double* dx, bool pairs_at_x = false) {
   ContactDev cd = contactdev(C);
   double cap = 1.0;
+  auto read_min = [&](double* m) {
+    JGS2_CUDA(cudaMemcpyAsync(m, C.res + R_CAP, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    C.sync();
+  };
   if (C.nplanes > 0) {
     k_cap_planes<<<red_grid(C.nsv * C.nplanes), kBlock, 0, C.stream>>>(
         cd, x, dx, C.partials + R_CAP * kMaxPartials, C.counters + R_CAP, C.res + R_CAP);
     C.check_launch();
     double m = 0;
-    JGS2_CUDA(cudaMemcpyAsync(&m, C.res + R_CAP, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
-    C.sync();
+    read_min(&m);
     if (std::isfinite(m)) cap = std::min(cap, 0.9 * m);
   }
   if (use_tri_grid(C)) {
-    // only pairs with dist < max rate / 0.9 can lower the cap below 1, and
-    // rate <= 2 max|dx|: a grid inflated by that radius is exact.
-    k_sv_maxstep<<<red_grid(C.nsv), kBlock, 0, C.stream>>>(cd, dx, C.partials + R_CAP * kMaxPartials,
-                                                           C.counters + R_CAP, C.res + R_CAP);
-    C.check_launch();
-    double M = 0;
-    JGS2_CUDA(cudaMemcpyAsync(&M, C.res + R_CAP, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
-    C.sync();
-    if (!(M > 0)) return std::max(cap, 0.0);
-    double r = 2.0 * M / 0.9 * (1.0 + 1e-6);
-    tri_grid_build(C, C.cap_grid, x, nullptr, 0.0, r, std::max(C.grid_cell, r));
-    k_cap_tris<<<red_grid(C.nsv), kBlock, 0, C.stream>>>(cd, grid_dev(C.cap_grid), x, dx,
+    if (pairs_at_x && C.npairs > 0) {
+      k_cap_pairtable<<<std::min(grid_for(C.npairs), 256), kBlock, 0, C.stream>>>(
+          C.npairs, C.pairs, dx, C.partials + R_CAP * kMaxPartials, C.counters + R_CAP, C.res + R_CAP);
+      C.check_launch();
+      double m = 0;
+      read_min(&m);
+      if (std::isfinite(m)) cap = std::min(cap, 0.9 * m);
+    }
+    if (!(cap > 0)) return std::max(cap, 0.0);
+    double sc = cap / 0.9 * (1.0 + 1e-6);
+    tri_grid_build(C, C.cap_grid, x, nullptr, 0.0, 1e-300, C.grid_cell, dx, sc, true);
+    k_cap_tris<<<red_grid(C.nsv), kBlock, 0, C.stream>>>(cd, grid_dev(C.cap_grid), x, dx, sc,
                                                          C.partials + R_CAP * kMaxPartials,
                                                          C.counters + R_CAP, C.res + R_CAP);
     C.check_launch();
     double m = 0;
-    JGS2_CUDA(cudaMemcpyAsync(&m, C.res + R_CAP, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
-    C.sync();
+    read_min(&m);
     if (std::isfinite(m)) cap = std::min(cap, 0.9 * m);
   }
   return std::max(cap, 0.0);

@@ -52,6 +52,8 @@ struct TriGrid {
   void* temp = nullptr;
   size_t temp_bytes = 0;
   double cell = 0.0;
+  int* over = nullptr;          // oversized triangles (allow_oversize builds)
+  int* n_over = nullptr;
 };
 
 // Device-side factor of the free-vertex rest Hessian (supernodal, ND order).
@@ -163,6 +165,8 @@ struct Ctx {
   double* xprev = nullptr;     // frame state (device frame driver)
   double* vel = nullptr;
   double* dz = nullptr;
+  double* xprev0 = nullptr;    // frame state saved by jgs2_set_frame_state
+  double* vel0 = nullptr;
   double gravity[3] = {0.0, 0.0, 0.0};
   bool rot_valid = false;
 
@@ -202,7 +206,16 @@ struct Ctx {
   double* pair_e = nullptr;    // per pair barrier energy
   int* flag_d = nullptr;       // infeasibility flag
   double grid_cell = 1.0;      // broadphase cell size
-  TriGrid pair_grid, cap_grid;
+  TriGrid pair_grid, cap_grid, cand_grid;
+  int* cand_v = nullptr;       // trial candidate pairs (vertex, triangle)
+  int* cand_t = nullptr;
+  int64_t cand_cap = 0;
+  int ncand = 0;               // -1: too many candidates, exact per-trial detection
+  long long* cand_cnt = nullptr;
+  long long* cand_off = nullptr;
+  double* tpart = nullptr;     // trial-batch partial sums
+  double* tres = nullptr;      // trial-batch results (elastic+inertia | barrier)
+  int* tflags = nullptr;       // trial-batch infeasibility flags
   void* scan_temp = nullptr;   // CUB scan workspace
   size_t scan_temp_bytes = 0;
 

@@ -11,6 +11,7 @@
 #include "factor.cuh"
 #include "sweep.cuh"
 #include "contact.cuh"
+#include "trials.cuh"
 
 using namespace jgs2;
 
@@ -27,6 +28,7 @@ jgs2::Ctx::~Ctx() {
   if (stream2) cudaStreamSynchronize(stream2);
   tri_grid_free(pair_grid);
   tri_grid_free(cap_grid);
+  tri_grid_free(cand_grid);
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
   if (stream2) cudaStreamDestroy(stream2);
@@ -193,6 +195,122 @@ void local_systems(Ctx& C, double* A_out, double* g_out, double* corr_out) {
   C.phase_end();
 }
 
+// Candidate cross-body (vertex, triangle) pairs for every trial position
+// x + gamma dx, gamma <= gmax (see trials.cuh).
+constexpr long long kCandBudget = 1LL << 26;
+
+void trial_candidates(Ctx& C, double gmax) {
+  C.ncand = 0;
+  if (!contact_active(C) || !use_tri_grid(C)) return;
+  ContactDev cd = contactdev(C);
+  k_sv_maxstep<<<red_grid(C.nsv), kBlock, 0, C.stream>>>(cd, C.dx, C.partials + R_AUX * kMaxPartials,
+                                                         C.counters + R_AUX, C.res + R_AUX);
+  C.check_launch();
+  double M = 0.0;
+  JGS2_CUDA(cudaMemcpyAsync(&M, C.res + R_AUX, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+  C.sync();
+  double r = C.dhat * (1.0 + 1e-6) + 2.0 * gmax * M * (1.0 + 1e-6) + 1e-300;
+  tri_grid_build(C, C.cand_grid, C.x, nullptr, 0.0, r, std::max(C.grid_cell, r));
+  TriGridDev gd = grid_dev(C.cand_grid);
+  if (!C.cand_cnt) {
+    C.cand_cnt = C.alloc<long long>(C.nsv + 1);
+    C.cand_off = C.alloc<long long>(C.nsv + 1);
+  }
+  k_cand_count<<<grid_for(C.nsv), kBlock, 0, C.stream>>>(cd, gd, C.x, C.cand_cnt);
+  C.check_launch();
+  JGS2_CUDA(cudaMemsetAsync(C.cand_cnt + C.nsv, 0, sizeof(long long), C.stream));
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, C.cand_cnt, C.cand_off, C.nsv + 1, C.stream);
+  if (tb > C.scan_temp_bytes) {
+    C.scan_temp = C.alloc<char>(tb);
+    C.scan_temp_bytes = tb;
+  }
+  JGS2_CUDA(cub::DeviceScan::ExclusiveSum(C.scan_temp, tb, C.cand_cnt, C.cand_off, C.nsv + 1, C.stream));
+  ++C.launches;
+  long long total = 0;
+  JGS2_CUDA(cudaMemcpyAsync(&total, C.cand_off + C.nsv, sizeof(long long), cudaMemcpyDeviceToHost, C.stream));
+  C.sync();
+  if (total > kCandBudget) {  // a large step inflated the radius: exact per-trial detection
+    C.ncand = -1;
+    return;
+  }
+  if (total > C.cand_cap) {
+    int64_t cap = std::max<int64_t>(2 * (int64_t)total, 4096);
+    C.cand_v = C.alloc<int>(cap);
+    C.cand_t = C.alloc<int>(cap);
+    C.cand_cap = cap;
+  }
+  k_cand_write<<<grid_for(C.nsv), kBlock, 0, C.stream>>>(cd, gd, C.x, C.cand_off, C.cand_v, C.cand_t);
+  C.check_launch();
+  C.ncand = (int)total;
+}
+
+// E(x + gamma_k dx) for n <= kTrialBatch gammas (host results), with
+// infeasibility flags (a barrier distance <= 0).
+void trial_energies(Ctx& C, const double* gam, int n, double* E, bool* infeasible) {
+  DevModel m = devmodel(C);
+  Gammas G;
+  G.n = n;
+  for (int k = 0; k < kTrialBatch; ++k) G.g[k] = k < n ? gam[k] : 0.0;
+  int grid = red_grid(std::max(C.ne, C.nv));
+  C.phase_begin(5, n * bytes_energy(C, true) / std::max(n, 1) + (n - 1) * 0.0);
+  k_energy_batch<<<grid, kBlock, 0, C.stream>>>(m, C.x, C.dx, G, C.z, C.h, C.tpart);
+  C.check_launch();
+  k_reduce_batch<<<1, kBlock, 0, C.stream>>>(C.tpart, grid, n, C.tres);
+  C.check_launch();
+  C.phase_end();
+  bool contact = contact_active(C);
+  if (contact && C.ncand < 0) {
+    // fallback: exact pair detection at every trial position (reference
+    // find_pairs(x_try)), one trial at a time
+    double* h = C.h_res;
+    JGS2_CUDA(cudaMemcpyAsync(h, C.tres, n * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    C.sync();
+    std::vector<double> el(h, h + n);
+    for (int k = 0; k < n; ++k) {
+      C.phase_begin(7, 0.0);
+      contact_find_pairs(C, C.x, C.dx, gam[k]);
+      bool inf = contact_infeasible(C);
+      double bar = 0.0;
+      if (C.npairs > 0) {
+        k_pair_energy_sum<<<std::min(grid_for(C.npairs), 64), kBlock, 0, C.stream>>>(
+            C.npairs, C.pairs, C.dhat, C.kappa, C.partials + R_AUX * kMaxPartials, C.counters + R_AUX,
+            C.res + R_AUX);
+        C.check_launch();
+        JGS2_CUDA(cudaMemcpyAsync(&bar, C.res + R_AUX, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+        C.sync();
+      }
+      C.phase_end();
+      E[k] = el[k] + bar;
+      infeasible[k] = inf;
+    }
+    return;
+  }
+  if (contact) {
+    C.phase_begin(7, 0.0);
+    ContactDev cd = contactdev(C);
+    int nb = std::max(1, std::min(red_grid((int64_t)C.nsv * C.nplanes + C.ncand), 1024));
+    JGS2_CUDA(cudaMemsetAsync(C.tflags, 0, kTrialBatch * sizeof(int), C.stream));
+    k_barrier_batch<<<nb, kBlock, 0, C.stream>>>(cd, C.ncand, C.cand_v, C.cand_t, C.x, C.dx, G,
+                                                 C.tpart + kTrialBatch * kMaxPartials, C.tflags);
+    C.check_launch();
+    k_reduce_batch<<<1, kBlock, 0, C.stream>>>(C.tpart + kTrialBatch * kMaxPartials, nb, n,
+                                               C.tres + kTrialBatch);
+    C.check_launch();
+    C.phase_end();
+  }
+  double* h = C.h_res;  // pinned scratch (>= 3 * kTrialBatch doubles)
+  JGS2_CUDA(cudaMemcpyAsync(h, C.tres, 2 * kTrialBatch * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+  JGS2_CUDA(cudaMemcpyAsync(h + 2 * kTrialBatch, C.tflags, kTrialBatch * sizeof(int), cudaMemcpyDeviceToHost,
+                            C.stream));
+  C.sync();
+  const int* fl = reinterpret_cast<const int*>(h + 2 * kTrialBatch);
+  for (int k = 0; k < n; ++k) {
+    E[k] = contact ? h[k] + h[kTrialBatch + k] : h[k];
+    infeasible[k] = contact && fl[k] != 0;
+  }
+}
+
 // One sweep on the device state. rot: compute rotations at x (outer_solve);
 // otherwise use the context's current rotations.
 void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
@@ -204,11 +322,7 @@ void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
     C.phase_begin(7, 0.0);
     contact_find_pairs(C, C.x, nullptr, 0.0);
     C.phase_end();
-  }
-  if (guard) {
-    launch_energy(C, nullptr, 0.0, R_EBEFORE);
-    if (contact_active(C) && contact_infeasible(C))
-      throw Error(JGS2_E_INFEASIBLE, "barrier distance <= 0 at the sweep start");
+    if (contact_infeasible(C)) throw Error(JGS2_E_INFEASIBLE, "barrier distance <= 0 at the sweep start");
   }
   vertex_pass(C, rot);
   if (contact_active(C)) {
@@ -228,43 +342,91 @@ void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
                                                           C.alpha_floor, C.dx);
   C.check_launch();
   C.phase_end();
-  double gamma = 1.0;
+  double gamma = 1.0, energy = 0.0;
   int halvings = 0;
-  bool have_trial_energy = false;
+  bool have_energy = false;
   int pairs_at_start = C.npairs;
+  int acts_ls = 0;
   if (guard) {
-    // global backtracking (local_solver.py:555-577)
+    // global backtracking (local_solver.py:555-577), trials in batches
     bool cap_needed = contact_active(C) && (C.npairs > 0 || C.nplanes > 0);
+    double cap = 1.0;
     if (cap_needed) {
       C.phase_begin(7, 0.0);
-      gamma = contact_step_cap(C, C.x, C.dx);
+      cap = contact_step_cap(C, C.x, C.dx, true);
       C.phase_end();
     }
-    int acts_ls = 0;
-    JGS2_CUDA(cudaMemcpyAsync(C.h_res + R_NSLOTS, C.ls_final + 2, sizeof(int), cudaMemcpyDeviceToHost, C.stream));
-    while (halvings <= C.max_halvings) {
-      launch_energy(C, C.dx, gamma, R_ENERGY);
-      JGS2_CUDA(cudaMemcpyAsync(C.h_res, C.res, R_NSLOTS * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
-      C.sync();
-      double e0 = C.h_res[R_EBEFORE], et = C.h_res[R_ENERGY];
-      if (contact_active(C) && contact_infeasible(C)) et = INFINITY;
-      if (et <= e0 + 1e-12 * std::fabs(e0)) { have_trial_energy = true; break; }
-      gamma *= 0.5;
-      halvings += 1;
+    JGS2_CUDA(cudaMemcpyAsync(&acts_ls, C.ls_final + 2, sizeof(int), cudaMemcpyDeviceToHost, C.stream));
+    if (contact_active(C)) {
+      C.phase_begin(7, 0.0);
+      trial_candidates(C, cap);
+      C.phase_end();
     }
-    memcpy(&acts_ls, C.h_res + R_NSLOTS, sizeof(int));
-    if (info) info->line_search_activations = acts_ls + halvings;
-  } else if (info) {
-    info->line_search_activations = 0;
+    const int MH = C.max_halvings;
+    std::vector<double> gam(MH + 2);
+    gam[0] = cap;
+    for (int j = 1; j <= MH + 1; ++j) gam[j] = gam[j - 1] * 0.5;
+    double e0 = 0.0;
+    int accepted = -1, next = 0;
+    double Eb[kTrialBatch];
+    bool bad[kTrialBatch];
+    double gb[kTrialBatch];
+    bool first = true;
+    while (accepted < 0 && next <= MH) {
+      int n = 0, base = next;
+      if (first) gb[n++] = 0.0;  // e_before rides in the first batch
+      int want = first ? 1 : kTrialBatch;
+      for (int q = 0; q < want && next <= MH; ++q) gb[n++] = gam[next++];
+      if (next > MH && n < kTrialBatch) gb[n++] = gam[MH + 1];  // floor energy (track_energy)
+      trial_energies(C, gb, n, Eb, bad);
+      int k0 = 0;
+      if (first) {
+        if (bad[0]) throw Error(JGS2_E_INFEASIBLE, "barrier distance <= 0 at the sweep start");
+        e0 = Eb[0];
+        k0 = 1;
+        first = false;
+      }
+      for (int k = k0; k < n; ++k) {
+        int j = base + (k - k0);
+        if (j > MH) {  // the floor position (only its energy is used)
+          energy = Eb[k];
+          have_energy = true;
+          break;
+        }
+        double et = bad[k] ? INFINITY : Eb[k];
+        if (et <= e0 + 1e-12 * std::fabs(e0)) {
+          accepted = j;
+          energy = Eb[k];
+          have_energy = true;
+          break;
+        }
+      }
+    }
+    if (accepted >= 0) {
+      halvings = accepted;
+      gamma = gam[accepted];
+    } else {
+      halvings = MH + 1;
+      gamma = gam[MH + 1];
+    }
   }
-  double e_trial = C.h_res[R_ENERGY];
   C.phase_begin(6, C.nv * 96.0);
   k_finalize<<<red_grid(C.nv), kBlock, 0, C.stream>>>(C.nv, C.x, C.dx, gamma, guard ? 1 : 0,
                                                        C.partials + R_DX2 * kMaxPartials,
                                                        C.counters + R_DX2, C.res);
   C.check_launch();
   C.phase_end();
-  if (C.track_energy && !have_trial_energy) launch_energy(C, nullptr, 0.0, R_ENERGY);
+  if (C.track_energy && !have_energy) {  // energy at the new x (gamma = 0 on the updated state)
+    double g0 = 0.0, E1;
+    bool b1;
+    if (contact_active(C)) {
+      C.phase_begin(7, 0.0);
+      trial_candidates(C, 0.0);
+      C.phase_end();
+    }
+    trial_energies(C, &g0, 1, &E1, &b1);
+    energy = b1 ? INFINITY : E1;
+  }
   JGS2_CUDA(cudaMemcpyAsync(C.h_res, C.res, R_NSLOTS * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
   int n_indef = 0;
   if (C.nuniq > 0)
@@ -272,12 +434,13 @@ void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
   C.sync();
   if (C.nuniq > 0) memcpy(&n_indef, C.h_res + R_NSLOTS + 1, sizeof(int));
   if (info) {
+    info->line_search_activations = guard ? acts_ls + halvings : 0;
     info->n_indefinite = n_indef;
     info->grad_sq = C.h_res[R_GRADSQ];
     info->grad_norm = std::sqrt(C.h_res[R_GRADSQ]);
     info->max_local_step = C.h_res[R_DXMAX];
     info->dx_norm = C.norm_scale * std::sqrt(C.h_res[R_DX2]);
-    info->energy = have_trial_energy ? e_trial : C.h_res[R_ENERGY];
+    info->energy = energy;
     info->halvings = halvings;
     info->n_pairs = pairs_at_start;
   }
@@ -311,7 +474,10 @@ jgs2_ctx* jgs2_create(int32_t device) {
     C.res = C.alloc<double>(R_NSLOTS);
     JGS2_CUDA(cudaMemset(C.counters, 0, R_NSLOTS * sizeof(unsigned)));
     JGS2_CUDA(cudaMemset(C.res, 0, R_NSLOTS * sizeof(double)));
-    JGS2_CUDA(cudaMallocHost(&C.h_res, 2 * R_NSLOTS * sizeof(double)));
+    JGS2_CUDA(cudaMallocHost(&C.h_res, 8 * R_NSLOTS * sizeof(double)));
+    C.tpart = C.alloc<double>(2 * (size_t)kTrialBatch * kMaxPartials);
+    C.tres = C.alloc<double>(2 * kTrialBatch);
+    C.tflags = C.alloc<int>(kTrialBatch);
     C.hess_count = C.alloc<int>(2);
     JGS2_CUDA(cudaStreamCreateWithFlags(&C.stream2, cudaStreamNonBlocking));
     JGS2_CUDA(cudaEventCreateWithFlags(&C.ev_fork, cudaEventDisableTiming));
@@ -708,8 +874,11 @@ int32_t jgs2_set_frame_state(jgs2_ctx* ctx, const double* x_prev, const double* 
     if (!(h > 0)) throw Error(JGS2_E_ARG, "h must be positive");
     size_t n = 3 * (size_t)C.nv;
     if (!C.xprev) { C.xprev = C.alloc<double>(n); C.vel = C.alloc<double>(n); C.dz = C.alloc<double>(n); }
+    if (!C.xprev0) { C.xprev0 = C.alloc<double>(n); C.vel0 = C.alloc<double>(n); }
     JGS2_CUDA(cudaMemcpyAsync(C.xprev, x_prev, n * sizeof(double), cudaMemcpyHostToDevice, C.stream));
     JGS2_CUDA(cudaMemcpyAsync(C.vel, v, n * sizeof(double), cudaMemcpyHostToDevice, C.stream));
+    JGS2_CUDA(cudaMemcpyAsync(C.xprev0, C.xprev, n * sizeof(double), cudaMemcpyDeviceToDevice, C.stream));
+    JGS2_CUDA(cudaMemcpyAsync(C.vel0, C.vel, n * sizeof(double), cudaMemcpyDeviceToDevice, C.stream));
     for (int c = 0; c < 3; ++c) C.gravity[c] = gravity ? gravity[c] : 0.0;
     C.h = h;
     C.sync();
@@ -727,6 +896,15 @@ int32_t jgs2_frame_begin(jgs2_ctx* ctx, double* cap_out) {
     C.check_launch();
     C.sync();
     if (cap_out) *cap_out = cap;
+  });
+}
+
+int32_t jgs2_frame_reset(jgs2_ctx* ctx) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (!C.xprev0) throw Error(JGS2_E_ARG, "frame state not set");
+    size_t n = 3 * (size_t)C.nv * sizeof(double);
+    JGS2_CUDA(cudaMemcpyAsync(C.xprev, C.xprev0, n, cudaMemcpyDeviceToDevice, C.stream));
+    JGS2_CUDA(cudaMemcpyAsync(C.vel, C.vel0, n, cudaMemcpyDeviceToDevice, C.stream));
   });
 }
 

@@ -369,16 +369,20 @@ class LocalSolver:
             out.append((it, conv))
         return out
 
-    def run_sweeps(self, budget):
+    def run_sweeps(self, budget, episode=None):
         """Continue the device-resident simulation for exactly ``budget``
         sweeps (frames end on convergence; a frame still open when the
-        budget runs out is resumed by the next call). Returns the list of
-        iteration counts of the frames completed in this call."""
+        budget runs out is resumed by the next call). With ``episode`` = E,
+        the frame state is restored (device copy) after every E frames.
+        Returns the list of iteration counts of the frames completed."""
         done = []
         left = budget
         cap = L.f64(1.0)
         while left > 0:
             if not getattr(self, "_frame_open", False):
+                if episode and getattr(self, "_episode_frames", 0) >= episode:
+                    self._call(self._lib.jgs2_frame_reset)
+                    self._episode_frames = 0
                 self._call(self._lib.jgs2_frame_begin, C_ref(cap))
                 self._frame_open, self._frame_iters = True, 0
             info = self.sweep_resident(refresh_rotations=True)
@@ -388,6 +392,7 @@ class LocalSolver:
                 self._call(self._lib.jgs2_frame_end)
                 done.append(self._frame_iters)
                 self._frame_open = False
+                self._episode_frames = getattr(self, "_episode_frames", 0) + 1
         return done
 
     def get_frame_state(self):

@@ -72,7 +72,7 @@ class Precompute:
                    cub_weights=np.array(cw, dtype=np.float64))
 
     @classmethod
-    def injected(cls, model, h_ref, samples=6, seed=0, weight_scale=0.05):
+    def injected(cls, model, h_ref, samples=6, seed=0, weight_scale=0.05, neighbor_scale=0.6):
         """Structurally valid synthetic precompute (bench scales only).
 
         * Gbar_v = -Hbar_vv (the vertex's own rest block, elastic + inertia):
@@ -136,7 +136,7 @@ class Precompute:
         x0 = np.asarray(model.rest_positions)
         ext = float(np.ptp(x0, axis=0).max()) or 1.0
         dist = np.linalg.norm(x0[keys] - x0[owner], axis=1) / ext
-        scale = np.where(keys == owner, 1.0, 0.6 * np.exp(-8.0 * dist))
+        scale = np.where(keys == owner, 1.0, neighbor_scale * np.exp(-8.0 * dist))
         vrows = np.zeros((keys.size, 3, 3))
         vrows[:, 0, 0] = vrows[:, 1, 1] = vrows[:, 2, 2] = scale
         cptr = np.zeros(nf + 1, dtype=np.int64)

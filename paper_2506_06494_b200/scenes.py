@@ -21,6 +21,13 @@ from .model import (BarrierParams, HalfSpace, MaterialParams, Model, SystemState
                     build_mesh, compute_z)
 
 H = 1.0 / 120.0
+# Contact scenes resolve the barrier layer: tol_dx * extent = 1% of dhat,
+# the ratio of the reference's cube_drop scene (tol 1e-3 on a 0.1 m scene,
+# dhat 1 cm; cube_drop.toml:10-22). A scene-level setting, like the TOML's.
+CONTACT_TOL = 2.5e-5
+# Contact benchmarks run fixed episodes of frames from the initial state
+# (the barrier layer otherwise collapses geometrically under floored sweeps).
+EPISODE = 6
 
 
 def cantilever(divisions=(24, 10, 7), extents=(1.2, 0.5, 0.35), young=1e6):
@@ -77,7 +84,8 @@ def puffer_ball_mesh(radius=0.5, cells=40, spikes=12, spike_amp=0.25, seed=0, ce
     return build_mesh(verts, tets)
 
 
-def puffer_balls(n_balls=1, cells=45, youngs=(2e7,), ncols=4, gap=0.2, walls=False, radius=0.5):
+def puffer_balls(n_balls=1, cells=45, youngs=(2e7,), ncols=4, gap=0.04, walls=False, radius=0.1,
+                 kappa=2e3):
     """C2 (1 ball on the ground plane) / C4 (10 balls in a glass tank).
 
     Balls stand in columns (ncols per layer, 2 x 2 footprint); the lowest
@@ -86,7 +94,8 @@ def puffer_balls(n_balls=1, cells=45, youngs=(2e7,), ncols=4, gap=0.2, walls=Fal
     barrier is active from the first sweep (plane and cross-body
     vertex-triangle pairs). Tank walls (C4) are 0.5 dhat outside the
     outermost vertices. dhat = 1% of the ball extent, kappa = 2e3
-    (cube_drop.toml:18-24). Materials cycle through ``youngs``.
+    (cube_drop.toml:18-24 shape, kappa scaled to the ball mass). Materials
+    cycle through ``youngs``.
     """
     meshes = [puffer_ball_mesh(radius=radius, cells=cells, seed=b) for b in range(n_balls)]
     ext = 2.0 * radius * 1.25
@@ -125,7 +134,9 @@ def puffer_balls(n_balls=1, cells=45, youngs=(2e7,), ncols=4, gap=0.2, walls=Fal
                    HalfSpace(np.array([hi[0], 0, 0]), np.array([-1.0, 0, 0])),
                    HalfSpace(np.array([0, 0, lo[2]]), np.array([0, 0, 1.0])),
                    HalfSpace(np.array([0, 0, hi[2]]), np.array([0, 0, -1.0]))]
-    return Model(bodies, planes=planes, barrier=BarrierParams(dhat=dhat, kappa=2e3))
+    # kappa scaled from cube_drop (0.125 kg cube, kappa 2e3) to ~500 kg balls so
+    # the barrier holds a ball on a few spike tips at ~dhat/2
+    return Model(bodies, planes=planes, barrier=BarrierParams(dhat=dhat, kappa=kappa))
 
 
 def predictor_state(model, state):
@@ -147,15 +158,20 @@ def build(name):
             "C3 stiff beam twist box_grid(160,40,26) 998,400 tets, E=2e7, no contact"
     if name == "c2":
         m = puffer_balls(1, cells=45, youngs=(2e7,))
+        m.tol_dx = CONTACT_TOL
+        m.episode_frames = EPISODE
         return m, predictor_state(m, SystemState.initial(m, H)), H, \
             f"C2 puffer ball {m.num_elements:,} tets on a ground plane, E=2e7, IPC barrier"
     if name == "c4":
         m = puffer_balls(10, cells=45, youngs=(1e6, 5e4), walls=True)
+        m.tol_dx = CONTACT_TOL
+        m.episode_frames = EPISODE
         return m, predictor_state(m, SystemState.initial(m, H)), H, \
             f"C4 ten puffer balls {m.num_elements:,} tets in a 5-plane tank, E 1e6/5e4, IPC"
     if name.startswith("c4s"):  # scaled-down C4 (tests / CPU samples): c4s<cells>
         cells = int(name[3:] or 12)
         m = puffer_balls(10, cells=cells, youngs=(1e6, 5e4), walls=True)
+        m.tol_dx = CONTACT_TOL
         return m, predictor_state(m, SystemState.initial(m, H)), H, f"C4 at {cells} cells/ball"
     if name.startswith("c3s"):  # scaled-down C3 for tests / CPU samples: c3s<k>
         k = int(name[3:] or 4)
