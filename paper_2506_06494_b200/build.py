@@ -16,8 +16,7 @@ CSRC = PKG / "csrc"
 LIBDIR = PKG / "lib"
 LIB = LIBDIR / "libjgs2.so"
 SOURCES = ["jgs2.cu", "symbolic.cpp"]
-HEADERS = ["context.cuh", "physics.cuh", "factor.cuh", "sweep.cuh", "contact.cuh",
-           "geometry.cuh", "symbolic.h"]
+HEADERS = sorted(p.name for p in CSRC.glob("*.cuh")) + ["symbolic.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

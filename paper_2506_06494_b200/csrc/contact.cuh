@@ -677,6 +677,8 @@ void contact_add_gradients(Ctx& C) {
   C.check_launch();
 }
 
+inline double hier_cap_min(Ctx& C, const double* x, const double* dx, double cap_ub);
+
 // feasibility_step_cap (assembly.py:263-291). pairs_at_x: the pair table
 // holds the pairs detected at this x (their d equal the reference's
 // closest-point distances bitwise) and gives an upper bound cap_ub; only
@@ -707,14 +709,19 @@ double contact_step_cap(Ctx& C, const double* x, const double* dx, bool pairs_at
       if (std::isfinite(m)) cap = std::min(cap, 0.9 * m);
     }
     if (!(cap > 0)) return std::max(cap, 0.0);
-    double sc = cap / 0.9 * (1.0 + 1e-6);
-    tri_grid_build(C, C.cap_grid, x, nullptr, 0.0, 1e-300, C.grid_cell, dx, sc, true);
-    k_cap_tris<<<red_grid(C.nsv), kBlock, 0, C.stream>>>(cd, grid_dev(C.cap_grid), x, dx, sc,
-                                                         C.partials + R_CAP * kMaxPartials,
-                                                         C.counters + R_CAP, C.res + R_CAP);
-    C.check_launch();
-    double m = 0;
-    read_min(&m);
+    {  // near-field pairs (within 2 cells): a cheap, usually tight upper bound
+      double rn = 2.0 * C.grid_cell;
+      tri_grid_build(C, C.cap_grid, x, nullptr, 0.0, rn, rn);
+      k_cap_tris<<<red_grid(C.nsv), kBlock, 0, C.stream>>>(cd, grid_dev(C.cap_grid), x, dx, 0.0,
+                                                           C.partials + R_CAP * kMaxPartials,
+                                                           C.counters + R_CAP, C.res + R_CAP);
+      C.check_launch();
+      double mn = 0;
+      read_min(&mn);
+      if (std::isfinite(mn)) cap = std::min(cap, 0.9 * mn);
+      if (!(cap > 0)) return std::max(cap, 0.0);
+    }
+    double m = hier_cap_min(C, x, dx, cap);
     if (std::isfinite(m)) cap = std::min(cap, 0.9 * m);
   }
   return std::max(cap, 0.0);

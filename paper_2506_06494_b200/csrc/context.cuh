@@ -56,6 +56,15 @@ struct TriGrid {
   int* n_over = nullptr;
 };
 
+// Sorted (key, id) entry list of the hierarchical cap grids (cap_hier.cuh).
+struct HierList {
+  long long cap = 0, n = 0;
+  long long *cnt = nullptr, *off = nullptr;
+  unsigned long long *ka = nullptr, *kb = nullptr;
+  int *ia = nullptr, *ib = nullptr;
+  int *over = nullptr, *n_over = nullptr;
+};
+
 // Device-side factor of the free-vertex rest Hessian (supernodal, ND order).
 struct Factor {
   bool ready = false;
@@ -207,6 +216,10 @@ struct Ctx {
   int* flag_d = nullptr;       // infeasibility flag
   double grid_cell = 1.0;      // broadphase cell size
   TriGrid pair_grid, cap_grid, cand_grid;
+  HierList hier_tri, hier_vtx;
+  int* hier_vlev = nullptr;
+  int* hier_tlev = nullptr;
+  unsigned* hier_masks = nullptr;
   int* cand_v = nullptr;       // trial candidate pairs (vertex, triangle)
   int* cand_t = nullptr;
   int64_t cand_cap = 0;

@@ -12,6 +12,7 @@
 #include "sweep.cuh"
 #include "contact.cuh"
 #include "trials.cuh"
+#include "cap_hier.cuh"
 
 using namespace jgs2;
 
