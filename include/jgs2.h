@@ -183,17 +183,20 @@ int32_t jgs2_find_pairs(jgs2_ctx* ctx, double* rows, int64_t capacity, int64_t* 
 int32_t jgs2_last_kernel_launches(jgs2_ctx* ctx, int64_t* launches);
 
 /* ---- measurement ------------------------------------------------------ */
-#define JGS2_NPHASES 8
+#define JGS2_NPHASES 11
 /* phases: 0 vertex pass (rotations + assembled field), 1 collect rhs,
  * 2 factor solve (forward + backward), 3 cubature element Hessians,
  * 4 local systems + line search, 5 energy evaluations, 6 update/finalize,
- * 7 contact (pairs, pair terms, caps). */
+ * 7 contact pairs at x (detection, pair terms, gradients), 8 sweep
+ * feasibility cap, 9 backtracking barrier trials (candidates + energies),
+ * 10 per-frame initial-guess feasibility cap. */
 int32_t jgs2_profile(jgs2_ctx* ctx, int32_t enable);
 /* accumulated device ms (CUDA events on the context stream), launch
  * counts and algorithmic bytes per phase since the last reset */
 int32_t jgs2_phase_stats(jgs2_ctx* ctx, double* ms, int64_t* launches, double* bytes);
 int32_t jgs2_phase_reset(jgs2_ctx* ctx);
-/* CUDA-event stopwatch on the context stream */
+/* CUDA-event stopwatch on the context stream; the window is also a
+ * cudaProfilerStart/Stop range (ncu --profile-from-start off) */
 int32_t jgs2_timer_start(jgs2_ctx* ctx);
 int32_t jgs2_timer_stop(jgs2_ctx* ctx, double* ms);
 /* pinned host buffers for the end-to-end path */

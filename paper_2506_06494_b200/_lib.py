@@ -28,7 +28,7 @@ EXPORTS = (
     "jgs2_frame_reset",
 )
 PHASES = ("vertex_pass", "collect_rhs", "factor_solve", "cubature_hessians", "local_systems",
-          "energy", "update", "contact")
+          "energy", "update", "contact_pairs", "contact_cap", "contact_trials", "frame_cap")
 
 
 def pinned_array(shape, dtype=np.float64):

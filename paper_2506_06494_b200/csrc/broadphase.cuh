@@ -120,6 +120,32 @@ __device__ __forceinline__ void grid_range(const TriGridDev& g, unsigned long lo
   *last = lo;
 }
 
+// Entries of one cell are in ascending object id order and objects are
+// numbered body by body, so the entries of body `bv` form one contiguous
+// run [o0, o1) of [q0, q1). Cross-body queries visit [q0, o0) and [o1, q1)
+// (still ascending) and never touch the own-body bulk of a cell, which is
+// nearly all of it for a surface vertex. body(q) = body of entry q.
+template <class BodyOf>
+__device__ __forceinline__ void own_run(long long q0, long long q1, int bv, BodyOf body, long long* o0,
+                                        long long* o1) {
+  if (q0 >= q1 || body(q0) > bv || body(q1 - 1) < bv) { *o0 = *o1 = q1; return; }
+  long long lo = q0, hi = q1;
+  while (lo < hi) { long long m = (lo + hi) >> 1; if (body(m) < bv) lo = m + 1; else hi = m; }
+  *o0 = lo;
+  hi = q1;
+  while (lo < hi) { long long m = (lo + hi) >> 1; if (body(m) <= bv) lo = m + 1; else hi = m; }
+  *o1 = lo;
+}
+
+// visit(entry) for the entries of [q0, q1) not of body bv, in order
+template <class BodyOf, class Visit>
+__device__ __forceinline__ void visit_cross(long long q0, long long q1, int bv, BodyOf body, Visit visit) {
+  long long o0, o1;
+  own_run(q0, q1, bv, body, &o0, &o1);
+  for (long long q = q0; q < o0; ++q) visit(q);
+  for (long long q = o1; q < q1; ++q) visit(q);
+}
+
 __device__ __forceinline__ unsigned long long point_key(const double* p, double inv_cell) {
   return cell_key(cell_coord(p[0], inv_cell), cell_coord(p[1], inv_cell), cell_coord(p[2], inv_cell));
 }

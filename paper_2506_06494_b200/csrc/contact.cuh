@@ -38,17 +38,21 @@ __global__ void k_pair_count(ContactDev cd, TriGridDev g, int use_grid, const do
     cnt[pl * cd.nsv + i] = (plane_dist(p, cd.planes + 6 * pl) < cd.dhat) ? 1 : 0;
   int hits = 0;
   int bv = cd.vbody[v];
-  long long q0 = 0, q1 = 0;
-  if (use_grid) grid_range(g, point_key(p, g.inv_cell), &q0, &q1);
-  else q1 = cd.nst;
-  for (long long q = q0; q < q1; ++q) {
-    int t = use_grid ? g.tris[q] : (int)q;
-    if (cd.tbody[t] == bv) continue;
+  auto test = [&](int t) {
     double a[3], b[3], c[3], bary[3];
     load_pos(x, dx, gamma, cd.st[3 * t], a);
     load_pos(x, dx, gamma, cd.st[3 * t + 1], b);
     load_pos(x, dx, gamma, cd.st[3 * t + 2], c);
     if (closest_point_tri(p, a, b, c, bary) < cd.dhat) ++hits;
+  };
+  if (use_grid) {
+    long long q0, q1;
+    grid_range(g, point_key(p, g.inv_cell), &q0, &q1);
+    visit_cross(q0, q1, bv, [&](long long q) { return cd.tbody[g.tris[q]]; },
+                [&](long long q) { test(g.tris[q]); });
+  } else {
+    for (int t = 0; t < cd.nst; ++t)
+      if (cd.tbody[t] != bv) test(t);
   }
   cnt[cd.nplanes * cd.nsv + i] = hits;
 }
@@ -112,12 +116,7 @@ __global__ void k_pair_write(ContactDev cd, TriGridDev g, int use_grid, const do
   }
   int o = off[cd.nplanes * cd.nsv + i];
   int bv = cd.vbody[v];
-  long long q0 = 0, q1 = 0;
-  if (use_grid) grid_range(g, point_key(p, g.inv_cell), &q0, &q1);
-  else q1 = cd.nst;
-  for (long long q = q0; q < q1; ++q) {
-    int t = use_grid ? g.tris[q] : (int)q;
-    if (cd.tbody[t] == bv) continue;
+  auto emit = [&](int t) {
     double a[3], b[3], c[3], bary[3];
     load_pos(x, dx, gamma, cd.st[3 * t], a);
     load_pos(x, dx, gamma, cd.st[3 * t + 1], b);
@@ -132,6 +131,15 @@ __global__ void k_pair_write(ContactDev cd, TriGridDev g, int use_grid, const do
       if (d <= 0.0) atomicOr(flag, 1);
       ++o;
     }
+  };
+  if (use_grid) {
+    long long q0, q1;
+    grid_range(g, point_key(p, g.inv_cell), &q0, &q1);
+    visit_cross(q0, q1, bv, [&](long long q) { return cd.tbody[g.tris[q]]; },
+                [&](long long q) { emit(g.tris[q]); });
+  } else {
+    for (int t = 0; t < cd.nst; ++t)
+      if (cd.tbody[t] != bv) emit(t);
   }
 }
 
@@ -460,53 +468,6 @@ __global__ void k_sv_maxstep(ContactDev cd, const double* dx, double* partials, 
   grid_reduce<OP_MAX>(mx, partials, counter, out);
 }
 
-// min over cross-body (vertex, triangle) pairs of dist / rate, rate =
-// |dx_v| + max corner |dx_t|. Only pairs with dist < rate / 0.9 can lower
-// the cap below 1; triangles are inflated by s_t / 0.9 and each vertex
-// scans the cells its box of half-size s_v / 0.9 overlaps (a pair with
-// dist < (s_v + s_t) / 0.9 always meets; repeats are harmless for a min).
-__global__ void k_cap_tris(ContactDev cd, TriGridDev g, const double* x, const double* dx, double vscale,
-                           double* partials, unsigned* counter, double* out) {
-  double mn = INFINITY;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cd.nsv; i += gridDim.x * blockDim.x) {
-    int v = cd.sv[i];
-    double p[3] = {x[3 * v], x[3 * v + 1], x[3 * v + 2]};
-    double sp = norm3_np(dx + 3 * v);
-    double rv = vscale * sp;
-    int bv = cd.vbody[v];
-    long long lo[3], hi[3];
-    for (int k = 0; k < 3; ++k) {
-      lo[k] = cell_coord(p[k] - rv, g.inv_cell);
-      hi[k] = cell_coord(p[k] + rv, g.inv_cell);
-    }
-    auto visit = [&](int t) {
-      if (cd.tbody[t] == bv) return;
-      int a0 = cd.st[3 * t], a1 = cd.st[3 * t + 1], a2 = cd.st[3 * t + 2];
-      double stt = fmax(fmax(norm3_np(dx + 3 * a0), norm3_np(dx + 3 * a1)), norm3_np(dx + 3 * a2));
-      double rate = sp + stt;
-      if (!(rate > 1e-30)) return;
-      double bary[3];
-      double d = closest_point_tri(p, x + 3 * a0, x + 3 * a1, x + 3 * a2, bary);
-      mn = fmin(mn, d / rate);
-    };
-    int no = *g.n_over;
-    for (int q = 0; q < no; ++q) visit(g.over[q]);
-    long long ncell = (hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1) * (hi[2] - lo[2] + 1);
-    if (!(ncell > 0 && ncell <= kMaxCellsPerTri)) {  // fast vertex: scan every triangle
-      for (int t = 0; t < cd.nst; ++t) visit(t);
-      continue;
-    }
-    for (long long ci = lo[0]; ci <= hi[0]; ++ci)
-      for (long long cj = lo[1]; cj <= hi[1]; ++cj)
-        for (long long ck = lo[2]; ck <= hi[2]; ++ck) {
-          long long q0, q1;
-          grid_range(g, cell_key(ci, cj, ck), &q0, &q1);
-          for (long long q = q0; q < q1; ++q) visit(g.tris[q]);
-        }
-  }
-  grid_reduce<OP_MIN>(mn, partials, counter, out);
-}
-
 // min over the active triangle pairs of the current pair table of d / rate
 // (an upper bound source for the cap: these pairs are among all pairs)
 __global__ void k_cap_pairtable(int npairs, const double* rows, const double* dx, double* partials,
@@ -709,18 +670,6 @@ double contact_step_cap(Ctx& C, const double* x, const double* dx, bool pairs_at
       if (std::isfinite(m)) cap = std::min(cap, 0.9 * m);
     }
     if (!(cap > 0)) return std::max(cap, 0.0);
-    {  // near-field pairs (within 2 cells): a cheap, usually tight upper bound
-      double rn = 2.0 * C.grid_cell;
-      tri_grid_build(C, C.cap_grid, x, nullptr, 0.0, rn, rn);
-      k_cap_tris<<<red_grid(C.nsv), kBlock, 0, C.stream>>>(cd, grid_dev(C.cap_grid), x, dx, 0.0,
-                                                           C.partials + R_CAP * kMaxPartials,
-                                                           C.counters + R_CAP, C.res + R_CAP);
-      C.check_launch();
-      double mn = 0;
-      read_min(&mn);
-      if (std::isfinite(mn)) cap = std::min(cap, 0.9 * mn);
-      if (!(cap > 0)) return std::max(cap, 0.0);
-    }
     double m = hier_cap_min(C, x, dx, cap);
     if (std::isfinite(m)) cap = std::min(cap, 0.9 * m);
   }

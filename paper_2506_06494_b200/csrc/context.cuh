@@ -56,7 +56,7 @@ struct TriGrid {
   int* n_over = nullptr;
 };
 
-// Sorted (key, id) entry list of the hierarchical cap grids (cap_hier.cuh).
+// Sorted (key, id) entry list of the hierarchical cap grids (hier_grid.cuh).
 struct HierList {
   long long cap = 0, n = 0;
   long long *cnt = nullptr, *off = nullptr;
@@ -215,7 +215,7 @@ struct Ctx {
   double* pair_e = nullptr;    // per pair barrier energy
   int* flag_d = nullptr;       // infeasibility flag
   double grid_cell = 1.0;      // broadphase cell size
-  TriGrid pair_grid, cap_grid, cand_grid;
+  TriGrid pair_grid;
   HierList hier_tri, hier_vtx;
   int* hier_vlev = nullptr;
   int* hier_tlev = nullptr;
@@ -234,7 +234,7 @@ struct Ctx {
 
   // measurement: per-phase CUDA-event intervals (accumulated at sync points)
   bool profiling = false;
-  static constexpr int kPhases = 8;
+  static constexpr int kPhases = 11;
   double phase_ms[kPhases] = {0};
   int64_t phase_launch[kPhases] = {0};
   double phase_bytes[kPhases] = {0};

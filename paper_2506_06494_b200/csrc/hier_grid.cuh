@@ -1,0 +1,507 @@
+// Two-sided hierarchical proximity search between surface vertices and
+// surface triangles of different bodies, for per-object search radii that
+// vary over orders of magnitude within one sweep (the exact collect can move
+// whole bodies while most of the surface barely moves).
+//
+// Each object carries a radius rho = b * s + pad, s = its step length |dx|
+// (a triangle: max over its corners). A (v, t) pair with
+//     dist(x_v, T(x)) < rho_v + rho_t
+// has overlapping boxes (v's box of half-size rho_v, t's AABB inflated by
+// rho_t), and every such pair meets in one hierarchical grid:
+//   * objects are binned by level l = ceil(log2(rho / cell)) (cell * 2^l is
+//     the cell size of grid l, so a box covers at most 4^3 cells of its own
+//     grid);
+//   * triangles of level <= L are inserted into triangle grid L; a vertex of
+//     level L queries triangle grid L;
+//   * vertices of level <= L are inserted into vertex grid L; a triangle of
+//     level L queries vertex grid L.
+// A pair is seen by the query of its higher-level object (both queries when
+// the levels tie). Objects whose own-level box would still cover more than
+// kHierMaxCells cells ("big", only for steps of kilometres) scan all
+// opposing objects instead.
+//
+// Two uses:
+//   * feasibility_step_cap (assembly.py:279-290), MIN mode: 0.9 min over
+//     cross pairs of dist / (s_v + s_t). Given an upper bound cap_ub, only
+//     pairs with dist < (cap_ub / 0.9)(s_v + s_t) can lower it: b = cap_ub /
+//     0.9, pad = 0. Repeats are harmless for a min.
+//   * the candidate superset of the batched backtracking trials
+//     (trials.cuh), LIST mode: every pair that can be within dhat at any
+//     x + gamma dx, gamma <= gamma_max, has dist(x) < dhat + gamma_max (s_v +
+//     s_t): b = gamma_max, pad = dhat / 2, and the exact distance at x
+//     filters the boxes. Each pair is emitted exactly once: the triangle
+//     side drops level ties, and within a query a pair is only reported in
+//     the grid cell holding the min corner of the intersection of the two
+//     boxes (a cell both objects cover).
+// Cell entries are in ascending object order and objects are numbered body
+// by body, so own-body runs are skipped without being read (own_run).
+#pragma once
+#include <chrono>
+#include "broadphase.cuh"
+#include "contact.cuh"
+
+namespace jgs2 {
+
+constexpr int kHierLevels = 14;
+constexpr long long kHierMaxCells = 4096;
+constexpr int kHierBig = 0x100;  // level flag: object scans all opposing objects
+
+enum HierMode { HIER_MIN = 0, HIER_COUNT = 1, HIER_WRITE = 2 };
+
+struct HierArgs {
+  ContactDev cd;
+  const double* x;
+  const double* dx;
+  double b;      // radius per unit step
+  double pad;    // radius added to every object
+  double cell;   // level-0 cell size
+  double dlim;   // LIST mode: keep pairs with dist < 2 pad + b (s_v + s_t) (slack included in b, pad)
+};
+
+__device__ __forceinline__ int hier_level(double rho, double cell) {
+  if (!(rho > cell)) return 0;
+  double q = ceil(log2(rho / cell));
+  if (!(q < kHierLevels - 1)) return kHierLevels - 1;  // also catches NaN
+  return q < 0 ? 0 : (int)q;
+}
+__device__ __forceinline__ unsigned long long hier_key(int level, long long ix, long long iy, long long iz) {
+  const long long off = 1LL << 19;
+  auto cl = [&](long long c) { return c < -off + 1 ? -off + 1 : (c > off - 2 ? off - 2 : c); };
+  return ((unsigned long long)level << 60) | ((unsigned long long)(cl(ix) + off) << 40) |
+         ((unsigned long long)(cl(iy) + off) << 20) | (unsigned long long)(cl(iz) + off);
+}
+
+__device__ __forceinline__ double tri_step(const double* dx, const int* st, int t) {
+  return fmax(fmax(norm3_np(dx + 3 * st[3 * t]), norm3_np(dx + 3 * st[3 * t + 1])),
+              norm3_np(dx + 3 * st[3 * t + 2]));
+}
+__device__ __forceinline__ void tri_box(const HierArgs& a, int t, double r, double* lo, double* hi) {
+  const int* st = a.cd.st;
+  for (int k = 0; k < 3; ++k) {
+    double p0 = a.x[3 * st[3 * t] + k], p1 = a.x[3 * st[3 * t + 1] + k], p2 = a.x[3 * st[3 * t + 2] + k];
+    lo[k] = fmin(p0, fmin(p1, p2)) - r;
+    hi[k] = fmax(p0, fmax(p1, p2)) + r;
+  }
+}
+__device__ __forceinline__ void vtx_box(const HierArgs& a, int v, double r, double* lo, double* hi) {
+  for (int k = 0; k < 3; ++k) { lo[k] = a.x[3 * v + k] - r; hi[k] = a.x[3 * v + k] + r; }
+}
+__device__ __forceinline__ double vtx_rho(const HierArgs& a, int v) { return a.b * norm3_np(a.dx + 3 * v) + a.pad; }
+__device__ __forceinline__ double tri_rho(const HierArgs& a, int t) { return a.b * tri_step(a.dx, a.cd.st, t) + a.pad; }
+
+__device__ __forceinline__ long long box_cells(const double* lo, const double* hi, double inv, long long* c0,
+                                               long long* c1) {
+  long long n = 1;
+  for (int k = 0; k < 3; ++k) {
+    c0[k] = (long long)floor(lo[k] * inv);
+    c1[k] = (long long)floor(hi[k] * inv);
+    long long w = c1[k] - c0[k] + 1;
+    if (!(w > 0) || w > kHierMaxCells) return kHierMaxCells + 1;
+    n *= w;
+    if (n > kHierMaxCells) return kHierMaxCells + 1;
+  }
+  return n;
+}
+__device__ __forceinline__ double level_inv(const HierArgs& a, int L) { return 1.0 / (a.cell * (double)(1LL << L)); }
+
+// per-object levels (+ kHierBig) and level occupancy masks
+__global__ void k_hier_levels(HierArgs a, int* vlev, int* tlev, unsigned* vmask, unsigned* tmask) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double lo[3], hi[3];
+  long long c0[3], c1[3];
+  if (i < a.cd.nsv) {
+    int v = a.cd.sv[i];
+    double r = vtx_rho(a, v);
+    int l = hier_level(r, a.cell);
+    vtx_box(a, v, r, lo, hi);
+    bool big = box_cells(lo, hi, level_inv(a, l), c0, c1) > kHierMaxCells;
+    vlev[i] = l | (big ? kHierBig : 0);
+    atomicOr(vmask, 1u << l);
+  }
+  if (i < a.cd.nst) {
+    double r = tri_rho(a, i);
+    int l = hier_level(r, a.cell);
+    tri_box(a, i, r, lo, hi);
+    bool big = box_cells(lo, hi, level_inv(a, l), c0, c1) > kHierMaxCells;
+    tlev[i] = l | (big ? kHierBig : 0);
+    atomicOr(tmask, 1u << l);
+  }
+}
+
+// grid entries of one object: the cells of its box in every grid L >= its
+// level that the opposing side occupies (big objects: none)
+template <bool WRITE>
+__device__ __forceinline__ long long hier_entries(const HierArgs& a, const double* lo, const double* hi, int lev,
+                                                  unsigned mask, int id, unsigned long long* keys, int* ids,
+                                                  long long o) {
+  if (lev & kHierBig) return 0;
+  long long n = 0;
+  for (int L = lev; L < kHierLevels; ++L) {
+    if (!((mask >> L) & 1u)) continue;
+    long long c0[3], c1[3];
+    long long nc = box_cells(lo, hi, level_inv(a, L), c0, c1);
+    if (WRITE)
+      for (long long i = c0[0]; i <= c1[0]; ++i)
+        for (long long j = c0[1]; j <= c1[1]; ++j)
+          for (long long k = c0[2]; k <= c1[2]; ++k) {
+            keys[o] = hier_key(L, i, j, k);
+            ids[o] = id;
+            ++o;
+          }
+    n += nc;
+  }
+  return n;
+}
+
+template <bool WRITE>
+__global__ void k_hier_tri_entries(HierArgs a, const int* tlev, const unsigned* vmask, const long long* off,
+                                   long long* cnt, unsigned long long* keys, int* ids) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= a.cd.nst) return;
+  double lo[3], hi[3];
+  tri_box(a, t, tri_rho(a, t), lo, hi);
+  long long n = hier_entries<WRITE>(a, lo, hi, tlev[t], *vmask, t, keys, ids, WRITE ? off[t] : 0);
+  if (!WRITE) cnt[t] = n;
+}
+
+template <bool WRITE>
+__global__ void k_hier_vtx_entries(HierArgs a, const int* vlev, const unsigned* tmask, const long long* off,
+                                   long long* cnt, unsigned long long* keys, int* ids) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.cd.nsv) return;
+  double lo[3], hi[3];
+  vtx_box(a, a.cd.sv[i], vtx_rho(a, a.cd.sv[i]), lo, hi);
+  long long n = hier_entries<WRITE>(a, lo, hi, vlev[i], *tmask, i, keys, ids, WRITE ? off[i] : 0);
+  if (!WRITE) cnt[i] = n;
+}
+
+__device__ __forceinline__ void key_range(const unsigned long long* keys, long long n, unsigned long long key,
+                                          long long* first, long long* last) {
+  long long lo = 0, hi = n;
+  while (lo < hi) { long long m = (lo + hi) >> 1; if (keys[m] < key) lo = m + 1; else hi = m; }
+  *first = lo;
+  hi = n;
+  while (lo < hi) { long long m = (lo + hi) >> 1; if (keys[m] <= key) lo = m + 1; else hi = m; }
+  *last = lo;
+}
+
+// dist(x_v, T(x)) and the pair's step rate s_v + s_t (cross-body pairs only)
+__device__ __forceinline__ double pair_dist(const HierArgs& a, int v, int t, double* rate) {
+  const int* st = a.cd.st;
+  int a0 = st[3 * t], a1 = st[3 * t + 1], a2 = st[3 * t + 2];
+  *rate = norm3_np(a.dx + 3 * v) + tri_step(a.dx, st, t);
+  double bary[3];
+  return closest_point_tri(a.x + 3 * v, a.x + 3 * a0, a.x + 3 * a1, a.x + 3 * a2, bary);
+}
+
+// the min-corner cell rule: is (p, q, s) the cell of max(lo_a, lo_b)?
+__device__ __forceinline__ bool owns_pair(const double* la, const double* lb, double inv, long long p, long long q,
+                                          long long s) {
+  return (long long)floor(fmax(la[0], lb[0]) * inv) == p && (long long)floor(fmax(la[1], lb[1]) * inv) == q &&
+         (long long)floor(fmax(la[2], lb[2]) * inv) == s;
+}
+
+struct HierOut {
+  double mn = INFINITY;   // MIN
+  long long n = 0;        // COUNT / WRITE
+  long long o = 0;        // WRITE cursor
+  int* cv = nullptr;
+  int* ct = nullptr;
+  template <int MODE>
+  __device__ __forceinline__ void take(const HierArgs& a, int v, int t) {
+    double rate;
+    double d = pair_dist(a, v, t, &rate);
+    if (MODE == HIER_MIN) {
+      if (rate > 1e-30) mn = fmin(mn, d / rate);
+    } else if (d < a.dlim + a.b * rate) {
+      if (MODE == HIER_WRITE) { cv[o] = v; ct[o] = t; ++o; }
+      ++n;
+    }
+  }
+};
+
+// vertex-side queries: triangle grid at the vertex's level (big: all triangles)
+template <int MODE>
+__global__ void k_hier_query_v(HierArgs a, const int* vlev, const int* tlev, const unsigned long long* tkeys,
+                               const int* tids, long long ntk, const long long* off, long long* cnt, int* cv,
+                               int* ct, double* partials, unsigned* counter, double* out) {
+  HierOut R;
+  R.cv = cv; R.ct = ct;
+  int i0 = blockIdx.x * blockDim.x + threadIdx.x;
+  int stride = MODE == HIER_MIN ? gridDim.x * blockDim.x : a.cd.nsv;
+  for (int i = i0; i < a.cd.nsv; i += stride) {
+    int v = a.cd.sv[i];
+    int bv = a.cd.vbody[v];
+    if (MODE == HIER_WRITE) R.o = off[i];
+    int lev = vlev[i];
+    if (lev & kHierBig) {  // pairs with big triangles are the triangle side's
+      for (int t = 0; t < a.cd.nst; ++t)
+        if (a.cd.tbody[t] != bv && !(tlev[t] & kHierBig)) R.take<MODE>(a, v, t);
+    } else {
+      double lo[3], hi[3], tl[3], th[3];
+      vtx_box(a, v, vtx_rho(a, v), lo, hi);
+      double inv = level_inv(a, lev);
+      long long c0[3], c1[3];
+      box_cells(lo, hi, inv, c0, c1);
+      for (long long p = c0[0]; p <= c1[0]; ++p)
+        for (long long q = c0[1]; q <= c1[1]; ++q)
+          for (long long s = c0[2]; s <= c1[2]; ++s) {
+            long long f, l;
+            key_range(tkeys, ntk, hier_key(lev, p, q, s), &f, &l);
+            visit_cross(f, l, bv, [&](long long e) { return a.cd.tbody[tids[e]]; }, [&](long long e) {
+              int t = tids[e];
+              if (MODE != HIER_MIN) {
+                tri_box(a, t, tri_rho(a, t), tl, th);
+                if (!owns_pair(lo, tl, inv, p, q, s)) return;
+              }
+              R.take<MODE>(a, v, t);
+            });
+          }
+    }
+    if (MODE == HIER_COUNT) cnt[i] = R.n, R.n = 0;
+  }
+  if (MODE == HIER_MIN) grid_reduce<OP_MIN>(R.mn, partials, counter, out);
+}
+
+// triangle-side queries: vertex grid at the triangle's level (big: all vertices)
+template <int MODE>
+__global__ void k_hier_query_t(HierArgs a, const int* vlev, const int* tlev, const unsigned long long* vkeys,
+                               const int* vids, long long nvk, const long long* off, long long* cnt, int* cv,
+                               int* ct, double* partials, unsigned* counter, double* out) {
+  HierOut R;
+  R.cv = cv; R.ct = ct;
+  int t0 = blockIdx.x * blockDim.x + threadIdx.x;
+  int stride = MODE == HIER_MIN ? gridDim.x * blockDim.x : a.cd.nst;
+  for (int t = t0; t < a.cd.nst; t += stride) {
+    int bt = a.cd.tbody[t];
+    if (MODE == HIER_WRITE) R.o = off[t];
+    int lev = tlev[t];
+    if (lev & kHierBig) {
+      for (int i = 0; i < a.cd.nsv; ++i) {
+        int v = a.cd.sv[i];
+        if (a.cd.vbody[v] != bt) R.take<MODE>(a, v, t);
+      }
+    } else {
+      double lo[3], hi[3], vl[3], vh[3];
+      tri_box(a, t, tri_rho(a, t), lo, hi);
+      double inv = level_inv(a, lev);
+      long long c0[3], c1[3];
+      box_cells(lo, hi, inv, c0, c1);
+      for (long long p = c0[0]; p <= c1[0]; ++p)
+        for (long long q = c0[1]; q <= c1[1]; ++q)
+          for (long long s = c0[2]; s <= c1[2]; ++s) {
+            long long f, l;
+            key_range(vkeys, nvk, hier_key(lev, p, q, s), &f, &l);
+            visit_cross(f, l, bt, [&](long long e) { return a.cd.vbody[a.cd.sv[vids[e]]]; }, [&](long long e) {
+              int i = vids[e];
+              int v = a.cd.sv[i];
+              if (MODE != HIER_MIN) {
+                if ((vlev[i] & ~kHierBig) >= lev) return;  // level tie: the vertex side has it
+                vtx_box(a, v, vtx_rho(a, v), vl, vh);
+                if (!owns_pair(lo, vl, inv, p, q, s)) return;
+              }
+              R.take<MODE>(a, v, t);
+            });
+          }
+    }
+    if (MODE == HIER_COUNT) cnt[t] = R.n, R.n = 0;
+  }
+  if (MODE == HIER_MIN) grid_reduce<OP_MIN>(R.mn, partials, counter, out);
+}
+
+inline void hier_alloc(Ctx& C, HierList& h, int nobj) {
+  if (h.cnt) return;
+  h.cnt = C.alloc<long long>(nobj + 1);
+  h.off = C.alloc<long long>(nobj + 1);
+}
+
+// exclusive scan of n+1 counts (last one zeroed) -> off; returns the total
+inline long long scan_counts(Ctx& C, long long* cnt, long long* off, long long n) {
+  JGS2_CUDA(cudaMemsetAsync(cnt + n, 0, sizeof(long long), C.stream));
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, n + 1, C.stream);
+  if (tb > C.scan_temp_bytes) { C.scan_temp = C.alloc<char>(tb); C.scan_temp_bytes = tb; }
+  JGS2_CUDA(cub::DeviceScan::ExclusiveSum(C.scan_temp, tb, cnt, off, n + 1, C.stream));
+  ++C.launches;
+  long long total = 0;
+  JGS2_CUDA(cudaMemcpyAsync(&total, off + n, sizeof(long long), cudaMemcpyDeviceToHost, C.stream));
+  C.sync();
+  return total;
+}
+
+template <class CountK, class WriteK>
+inline void hier_build(Ctx& C, HierList& h, int nobj, CountK count, WriteK write) {
+  hier_alloc(C, h, nobj);
+  count(h);
+  C.check_launch();
+  long long total = scan_counts(C, h.cnt, h.off, nobj);
+  if (total < 0 || total > (long long)INT32_MAX)
+    throw Error(-2, "hierarchical grid: entry count " + std::to_string(total) + " out of range");
+  if (total > h.cap) {
+    long long cap = std::max<long long>(total + total / 2, 4096);
+    h.ka = C.alloc<unsigned long long>(cap); h.kb = C.alloc<unsigned long long>(cap);
+    h.ia = C.alloc<int>(cap); h.ib = C.alloc<int>(cap);
+    h.cap = cap;
+  }
+  h.n = total;
+  if (total == 0) return;
+  write(h);
+  C.check_launch();
+  size_t sb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, sb, h.ka, h.kb, h.ia, h.ib, (int)total, 0, 64, C.stream);
+  if (sb > C.scan_temp_bytes) { C.scan_temp = C.alloc<char>(sb); C.scan_temp_bytes = sb; }
+  JGS2_CUDA(cub::DeviceRadixSort::SortPairs(C.scan_temp, sb, h.ka, h.kb, h.ia, h.ib, (int)total, 0, 64,
+                                            C.stream));
+  ++C.launches;
+}
+
+// levels + both grids for radii b * s + pad
+inline void hier_prepare(Ctx& C, const HierArgs& a) {
+  if (!C.hier_vlev) {
+    C.hier_vlev = C.alloc<int>(C.nsv + 1);
+    C.hier_tlev = C.alloc<int>(C.nst + 1);
+    C.hier_masks = C.alloc<unsigned>(2);
+  }
+  JGS2_CUDA(cudaMemsetAsync(C.hier_masks, 0, 2 * sizeof(unsigned), C.stream));
+  int nmax = std::max(C.nsv, C.nst);
+  k_hier_levels<<<grid_for(nmax), kBlock, 0, C.stream>>>(a, C.hier_vlev, C.hier_tlev, C.hier_masks,
+                                                         C.hier_masks + 1);
+  C.check_launch();
+  hier_build(C, C.hier_tri, C.nst,
+             [&](HierList& h) {
+               k_hier_tri_entries<false><<<grid_for(C.nst), kBlock, 0, C.stream>>>(
+                   a, C.hier_tlev, C.hier_masks, nullptr, h.cnt, nullptr, nullptr);
+             },
+             [&](HierList& h) {
+               k_hier_tri_entries<true><<<grid_for(C.nst), kBlock, 0, C.stream>>>(
+                   a, C.hier_tlev, C.hier_masks, h.off, nullptr, h.ka, h.ia);
+             });
+  hier_build(C, C.hier_vtx, C.nsv,
+             [&](HierList& h) {
+               k_hier_vtx_entries<false><<<grid_for(C.nsv), kBlock, 0, C.stream>>>(
+                   a, C.hier_vlev, C.hier_masks + 1, nullptr, h.cnt, nullptr, nullptr);
+             },
+             [&](HierList& h) {
+               k_hier_vtx_entries<true><<<grid_for(C.nsv), kBlock, 0, C.stream>>>(
+                   a, C.hier_vlev, C.hier_masks + 1, h.off, nullptr, h.ka, h.ia);
+             });
+}
+
+// min over cross-body pairs of dist / rate among the pairs with rate < b
+// (those whose boxes of radius b s overlap); INFINITY if there are none
+inline double hier_min_ratio(Ctx& C, const double* x, const double* dx, double b) {
+  HierArgs a;
+  a.cd = contactdev(C);
+  a.x = x;
+  a.dx = dx;
+  a.b = b;
+  a.pad = 0.0;
+  a.cell = C.grid_cell;
+  a.dlim = 0.0;
+  bool dbg = getenv("JGS2_DEBUG_HIER") != nullptr;
+  auto now = [&]() { if (dbg) C.sync(); return std::chrono::steady_clock::now(); };
+  auto t0 = now();
+  hier_prepare(C, a);
+  auto t1 = now();
+  const HierList& T = C.hier_tri;
+  const HierList& V = C.hier_vtx;
+  double* part = C.partials + R_CAP * kMaxPartials;
+  double m[2] = {INFINITY, INFINITY};
+  k_hier_query_v<HIER_MIN><<<red_grid(C.nsv), kBlock, 0, C.stream>>>(
+      a, C.hier_vlev, C.hier_tlev, T.kb, T.ib, T.n, nullptr, nullptr, nullptr, nullptr, part,
+      C.counters + R_CAP, C.res + R_CAP);
+  C.check_launch();
+  JGS2_CUDA(cudaMemcpyAsync(&m[0], C.res + R_CAP, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+  k_hier_query_t<HIER_MIN><<<red_grid(C.nst), kBlock, 0, C.stream>>>(
+      a, C.hier_vlev, C.hier_tlev, V.kb, V.ib, V.n, nullptr, nullptr, nullptr, nullptr, part,
+      C.counters + R_CAP, C.res + R_CAP);
+  C.check_launch();
+  JGS2_CUDA(cudaMemcpyAsync(&m[1], C.res + R_CAP, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+  C.sync();
+  if (dbg) {
+    auto t2 = now();
+    unsigned mk[2];
+    JGS2_CUDA(cudaMemcpy(mk, C.hier_masks, sizeof(mk), cudaMemcpyDeviceToHost));
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    fprintf(stderr, "hier_min_ratio b=%.3e entries tri=%lld vtx=%lld masks v=%x t=%x m=%.3e %.3e ms prep %.2f q %.2f\n",
+            a.b, T.n, V.n, mk[0], mk[1], m[0], m[1], ms(t0, t1), ms(t1, t2));
+  }
+  return std::fmin(m[0], m[1]);
+}
+
+// min over cross-body pairs of dist / rate among pairs that can lower
+// cap_ub (ratio < cap_ub / 0.9). The search radius grows geometrically from
+// one that keeps every box within 2 level-0 cells: a round with radius
+// factor b examines every pair of ratio < b, so the first round that finds
+// one has the exact minimum. Steps can be huge (the exact collect spreads
+// barrier forces over whole bodies), and the limiting pair is then found
+// with small boxes instead of body-sized ones.
+inline double hier_cap_min(Ctx& C, const double* x, const double* dx, double cap_ub) {
+  double bmax = cap_ub / 0.9 * (1.0 + 1e-6);
+  ContactDev cd = contactdev(C);
+  k_sv_maxstep<<<red_grid(C.nsv), kBlock, 0, C.stream>>>(cd, dx, C.partials + R_AUX * kMaxPartials,
+                                                         C.counters + R_AUX, C.res + R_AUX);
+  C.check_launch();
+  double smax = 0.0;
+  JGS2_CUDA(cudaMemcpyAsync(&smax, C.res + R_AUX, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+  C.sync();
+  if (!(smax > 0.0)) return INFINITY;  // nothing moves: no pair lowers the cap
+  double b = std::isfinite(smax) ? std::min(bmax, 2.0 * C.grid_cell / smax) : bmax;
+  for (;;) {
+    double m = hier_min_ratio(C, x, dx, b);
+    if (m < b || b >= bmax) return m;
+    b = std::min(bmax, 4.0 * b);
+  }
+}
+
+// Cross-body (vertex, triangle) pairs that can be within dhat at some
+// x + gamma dx, gamma <= gmax, each exactly once, into (cv, ct). Returns the
+// count, or -1 (nothing written) when it exceeds `budget`.
+inline long long hier_candidates(Ctx& C, const double* x, const double* dx, double gmax, long long budget) {
+  HierArgs a;
+  a.cd = contactdev(C);
+  a.x = x;
+  a.dx = dx;
+  a.b = gmax * (1.0 + 1e-6);
+  a.pad = 0.5 * C.dhat * (1.0 + 1e-6);
+  a.cell = C.grid_cell;
+  a.dlim = 2.0 * a.pad;
+  hier_prepare(C, a);
+  const HierList& T = C.hier_tri;
+  const HierList& V = C.hier_vtx;
+  long long nobj = (long long)C.nsv + C.nst;
+  if (!C.cand_cnt) {
+    C.cand_cnt = C.alloc<long long>(nobj + 1);
+    C.cand_off = C.alloc<long long>(nobj + 1);
+  }
+  long long* cv_cnt = C.cand_cnt;
+  long long* ct_cnt = C.cand_cnt + C.nsv;
+  k_hier_query_v<HIER_COUNT><<<grid_for(C.nsv), kBlock, 0, C.stream>>>(
+      a, C.hier_vlev, C.hier_tlev, T.kb, T.ib, T.n, nullptr, cv_cnt, nullptr, nullptr, nullptr, nullptr,
+      nullptr);
+  C.check_launch();
+  k_hier_query_t<HIER_COUNT><<<grid_for(C.nst), kBlock, 0, C.stream>>>(
+      a, C.hier_vlev, C.hier_tlev, V.kb, V.ib, V.n, nullptr, ct_cnt, nullptr, nullptr, nullptr, nullptr,
+      nullptr);
+  C.check_launch();
+  long long total = scan_counts(C, C.cand_cnt, C.cand_off, nobj);
+  if (total > budget) return -1;
+  if (total > C.cand_cap) {
+    int64_t cap = std::max<int64_t>(2 * (int64_t)total, 4096);
+    C.cand_v = C.alloc<int>(cap);
+    C.cand_t = C.alloc<int>(cap);
+    C.cand_cap = cap;
+  }
+  if (total == 0) return 0;
+  k_hier_query_v<HIER_WRITE><<<grid_for(C.nsv), kBlock, 0, C.stream>>>(
+      a, C.hier_vlev, C.hier_tlev, T.kb, T.ib, T.n, C.cand_off, nullptr, C.cand_v, C.cand_t, nullptr,
+      nullptr, nullptr);
+  C.check_launch();
+  k_hier_query_t<HIER_WRITE><<<grid_for(C.nst), kBlock, 0, C.stream>>>(
+      a, C.hier_vlev, C.hier_tlev, V.kb, V.ib, V.n, C.cand_off + C.nsv, nullptr, C.cand_v, C.cand_t,
+      nullptr, nullptr, nullptr);
+  C.check_launch();
+  return total;
+}
+
+}  // namespace jgs2

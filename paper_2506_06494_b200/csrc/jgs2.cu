@@ -1,5 +1,6 @@
 // C-ABI implementation of the B200-native JGS2 runtime iteration.
 // See include/jgs2.h for the contract and DESIGN.md for the data layout.
+#include <cuda_profiler_api.h>
 #include "../../include/jgs2.h"
 
 #include <algorithm>
@@ -12,7 +13,7 @@
 #include "sweep.cuh"
 #include "contact.cuh"
 #include "trials.cuh"
-#include "cap_hier.cuh"
+#include "hier_grid.cuh"
 
 using namespace jgs2;
 
@@ -28,8 +29,6 @@ jgs2::Ctx::~Ctx() {
   if (cusolver) cusolverDnDestroy(cusolver);
   if (stream2) cudaStreamSynchronize(stream2);
   tri_grid_free(pair_grid);
-  tri_grid_free(cap_grid);
-  tri_grid_free(cand_grid);
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
   if (stream2) cudaStreamDestroy(stream2);
@@ -116,7 +115,7 @@ void launch_energy(Ctx& C, const double* dx, double gamma, int slot) {
   C.check_launch();
   C.phase_end();
   if (contact_active(C)) {
-    C.phase_begin(7, 0.0);
+    C.phase_begin(9, 0.0);
     contact_energy_at(C, dx, gamma, slot);
     C.phase_end();
   }
@@ -203,47 +202,8 @@ constexpr long long kCandBudget = 1LL << 26;
 void trial_candidates(Ctx& C, double gmax) {
   C.ncand = 0;
   if (!contact_active(C) || !use_tri_grid(C)) return;
-  ContactDev cd = contactdev(C);
-  k_sv_maxstep<<<red_grid(C.nsv), kBlock, 0, C.stream>>>(cd, C.dx, C.partials + R_AUX * kMaxPartials,
-                                                         C.counters + R_AUX, C.res + R_AUX);
-  C.check_launch();
-  double M = 0.0;
-  JGS2_CUDA(cudaMemcpyAsync(&M, C.res + R_AUX, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
-  C.sync();
-  double r = C.dhat * (1.0 + 1e-6) + 2.0 * gmax * M * (1.0 + 1e-6) + 1e-300;
-  tri_grid_build(C, C.cand_grid, C.x, nullptr, 0.0, r, std::max(C.grid_cell, r));
-  TriGridDev gd = grid_dev(C.cand_grid);
-  if (!C.cand_cnt) {
-    C.cand_cnt = C.alloc<long long>(C.nsv + 1);
-    C.cand_off = C.alloc<long long>(C.nsv + 1);
-  }
-  k_cand_count<<<grid_for(C.nsv), kBlock, 0, C.stream>>>(cd, gd, C.x, C.cand_cnt);
-  C.check_launch();
-  JGS2_CUDA(cudaMemsetAsync(C.cand_cnt + C.nsv, 0, sizeof(long long), C.stream));
-  size_t tb = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tb, C.cand_cnt, C.cand_off, C.nsv + 1, C.stream);
-  if (tb > C.scan_temp_bytes) {
-    C.scan_temp = C.alloc<char>(tb);
-    C.scan_temp_bytes = tb;
-  }
-  JGS2_CUDA(cub::DeviceScan::ExclusiveSum(C.scan_temp, tb, C.cand_cnt, C.cand_off, C.nsv + 1, C.stream));
-  ++C.launches;
-  long long total = 0;
-  JGS2_CUDA(cudaMemcpyAsync(&total, C.cand_off + C.nsv, sizeof(long long), cudaMemcpyDeviceToHost, C.stream));
-  C.sync();
-  if (total > kCandBudget) {  // a large step inflated the radius: exact per-trial detection
-    C.ncand = -1;
-    return;
-  }
-  if (total > C.cand_cap) {
-    int64_t cap = std::max<int64_t>(2 * (int64_t)total, 4096);
-    C.cand_v = C.alloc<int>(cap);
-    C.cand_t = C.alloc<int>(cap);
-    C.cand_cap = cap;
-  }
-  k_cand_write<<<grid_for(C.nsv), kBlock, 0, C.stream>>>(cd, gd, C.x, C.cand_off, C.cand_v, C.cand_t);
-  C.check_launch();
-  C.ncand = (int)total;
+  long long n = hier_candidates(C, C.x, C.dx, gmax, kCandBudget);
+  C.ncand = n < 0 ? -1 : (int)n;  // -1: a huge step, exact per-trial detection
 }
 
 // E(x + gamma_k dx) for n <= kTrialBatch gammas (host results), with
@@ -269,7 +229,7 @@ void trial_energies(Ctx& C, const double* gam, int n, double* E, bool* infeasibl
     C.sync();
     std::vector<double> el(h, h + n);
     for (int k = 0; k < n; ++k) {
-      C.phase_begin(7, 0.0);
+      C.phase_begin(9, 0.0);
       contact_find_pairs(C, C.x, C.dx, gam[k]);
       bool inf = contact_infeasible(C);
       double bar = 0.0;
@@ -288,7 +248,7 @@ void trial_energies(Ctx& C, const double* gam, int n, double* E, bool* infeasibl
     return;
   }
   if (contact) {
-    C.phase_begin(7, 0.0);
+    C.phase_begin(9, 0.0);
     ContactDev cd = contactdev(C);
     int nb = std::max(1, std::min(red_grid((int64_t)C.nsv * C.nplanes + C.ncand), 1024));
     JGS2_CUDA(cudaMemsetAsync(C.tflags, 0, kTrialBatch * sizeof(int), C.stream));
@@ -353,13 +313,13 @@ void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
     bool cap_needed = contact_active(C) && (C.npairs > 0 || C.nplanes > 0);
     double cap = 1.0;
     if (cap_needed) {
-      C.phase_begin(7, 0.0);
+      C.phase_begin(8, 0.0);
       cap = contact_step_cap(C, C.x, C.dx, true);
       C.phase_end();
     }
     JGS2_CUDA(cudaMemcpyAsync(&acts_ls, C.ls_final + 2, sizeof(int), cudaMemcpyDeviceToHost, C.stream));
     if (contact_active(C)) {
-      C.phase_begin(7, 0.0);
+      C.phase_begin(9, 0.0);
       trial_candidates(C, cap);
       C.phase_end();
     }
@@ -421,7 +381,7 @@ void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
     double g0 = 0.0, E1;
     bool b1;
     if (contact_active(C)) {
-      C.phase_begin(7, 0.0);
+      C.phase_begin(9, 0.0);
       trial_candidates(C, 0.0);
       C.phase_end();
     }
@@ -892,7 +852,12 @@ int32_t jgs2_frame_begin(jgs2_ctx* ctx, double* cap_out) {
     k_compute_z<<<grid_for(C.nv), kBlock, 0, C.stream>>>(C.nv, C.xprev, C.vel, C.h, C.gravity[0],
                                                          C.gravity[1], C.gravity[2], C.fixed, C.z, C.dz);
     C.check_launch();
-    double cap = contact_active(C) ? contact_step_cap(C, C.xprev, C.dz) : 1.0;
+    double cap = 1.0;
+    if (contact_active(C)) {
+      C.phase_begin(10, 0.0);
+      cap = contact_step_cap(C, C.xprev, C.dz);
+      C.phase_end();
+    }
     k_init_x<<<grid_for(3 * (int64_t)C.nv), kBlock, 0, C.stream>>>(C.nv, C.xprev, C.dz, cap, C.x);
     C.check_launch();
     C.sync();
@@ -1047,6 +1012,7 @@ int32_t jgs2_timer_start(jgs2_ctx* ctx) {
   return guarded(ctx, [&](Ctx& C) {
     if (!C.tstart) { JGS2_CUDA(cudaEventCreate(&C.tstart)); JGS2_CUDA(cudaEventCreate(&C.tstop)); }
     JGS2_CUDA(cudaEventRecord(C.tstart, C.stream));
+    cudaProfilerStart();  // profiler range = the timed window (ncu --profile-from-start off)
   });
 }
 
@@ -1055,6 +1021,7 @@ int32_t jgs2_timer_stop(jgs2_ctx* ctx, double* ms) {
     if (!C.tstart) throw Error(JGS2_E_ARG, "timer not started");
     JGS2_CUDA(cudaEventRecord(C.tstop, C.stream));
     JGS2_CUDA(cudaEventSynchronize(C.tstop));
+    cudaProfilerStop();
     float f = 0.f;
     JGS2_CUDA(cudaEventElapsedTime(&f, C.tstart, C.tstop));
     *ms = f;

@@ -8,10 +8,10 @@
 // inertia terms per element/vertex for every gamma, and the barrier over
 //   * all (surface vertex, plane) pairs, and
 //   * a candidate list of cross-body (vertex, triangle) pairs built once per
-//     sweep from a grid inflated by dhat + 2 gamma_max max|dx|: a pair at
-//     distance < dhat at any trial position is within that radius at x, so
-//     the candidates contain every trial's exact pair set; each trial keeps
-//     the candidates whose distance (reference rounding) is < dhat.
+//     sweep (hier_grid.cuh): a pair at distance < dhat at any trial
+//     position has dist(x) < dhat + gamma_max (s_v + s_t), so the candidates
+//     contain every trial's exact pair set; each trial keeps the candidates
+//     whose distance (reference rounding) is < dhat.
 // A trial with any active distance <= 0 is infeasible (E = inf).
 #pragma once
 #include "contact.cuh"
@@ -158,36 +158,6 @@ __global__ void k_reduce_batch(const double* partials, int nblocks, int n, doubl
     acc = block_reduce<OP_SUM>(acc);
     if (threadIdx.x == 0) out[k] = acc;
     __syncthreads();
-  }
-}
-
-// candidate (vertex, triangle) list from a grid (cross-body only)
-__global__ void k_cand_count(ContactDev cd, TriGridDev g, const double* x, long long* cnt) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= cd.nsv) return;
-  int v = cd.sv[i];
-  int bv = cd.vbody[v];
-  long long q0, q1;
-  grid_range(g, point_key(x + 3 * v, g.inv_cell), &q0, &q1);
-  long long c = 0;
-  for (long long q = q0; q < q1; ++q) c += (cd.tbody[g.tris[q]] != bv);
-  cnt[i] = c;
-}
-__global__ void k_cand_write(ContactDev cd, TriGridDev g, const double* x, const long long* off, int* cv,
-                             int* ct) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= cd.nsv) return;
-  int v = cd.sv[i];
-  int bv = cd.vbody[v];
-  long long q0, q1;
-  grid_range(g, point_key(x + 3 * v, g.inv_cell), &q0, &q1);
-  long long o = off[i];
-  for (long long q = q0; q < q1; ++q) {
-    int t = g.tris[q];
-    if (cd.tbody[t] == bv) continue;
-    cv[o] = v;
-    ct[o] = t;
-    ++o;
   }
 }
 

@@ -234,9 +234,10 @@ class LocalSolver:
 
     def phase_stats(self):
         """{phase: (device ms, kernel launches, algorithmic bytes)}."""
-        ms = np.zeros(8)
-        n = np.zeros(8, dtype=np.int64)
-        by = np.zeros(8)
+        k = len(L.PHASES)
+        ms = np.zeros(k)
+        n = np.zeros(k, dtype=np.int64)
+        by = np.zeros(k)
         self._call(self._lib.jgs2_phase_stats, L.ptr(ms, L.f64), L.ptr(n, L.i64), L.ptr(by, L.f64))
         return {p: (float(ms[i]), int(n[i]), float(by[i])) for i, p in enumerate(L.PHASES)}
 
