@@ -9,7 +9,7 @@ local line search and the sweep-level backtracking guard), i.e. one
 host memory, x, dx out, every step). ``--impl reference`` times the CPU
 oracle port of the reference (numpy/SciPy, oracle/) on a bounded sample.
 
-Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3]
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4|c3|c2|c1]
 """
 
 import argparse
@@ -110,14 +110,24 @@ def max_over_ranks(dist, v):
 # ----------------------------------------------------------------- CPU oracle
 def cpu_sample(config, steps=3, budget_s=25.0):
     """Time the CPU oracle port (oracle/jgs2_oracle.py) on a bounded sample
-    of the workload: the same scene construction scaled down to ~10K tets,
-    injected precompute, ``steps`` sweeps; returns seconds/sweep scaled
-    linearly in element count to the full workload (measured 84-89
-    us/tet/sweep is linear in ne)."""
+    of the workload and extrapolate to the full scene; returns (seconds per
+    sweep at full size, description).
+
+    * elastic sweep: the same construction scaled down to ~10K tets
+      (injected precompute), ``steps`` sweeps, median s/sweep scaled linearly
+      in element count (84-89 us/tet/sweep is linear in ne, SURVEY App. C3);
+    * contact scenes (the reference's brute-force proximity
+      needs n_sv x n_st x 3 doubles at C4, petabytes, so it is not runnable):
+      one brute-force find_pairs on the 10-body scene at 6 cells/ball, scaled
+      by n_sv * n_st, times the 3 calls a sweep makes at least (pairs at x,
+      one backtracking trial, the tracked energy; local_solver.py:612, 567,
+      712) -- a lower bound on the reference's contact cost.
+    """
     from oracle import jgs2_oracle as orc
     from paper_2506_06494_b200 import scenes
     from paper_2506_06494_b200.precompute import Precompute
-    name = {"c3": "c3s4", "c1": "c1"}.get(config, "c3s4")
+    m_full, _, _, _ = scenes.build(config)
+    name = "c1" if config == "c1" else "c3s4"
     m, st, h, _ = scenes.build(name)
     pre = Precompute.injected(m, h, samples=6, seed=0)
     solver = orc.OracleSolver(m, pre, h, orc.OracleConfig(max_outer=steps))
@@ -130,8 +140,36 @@ def cpu_sample(config, steps=3, budget_s=25.0):
         times.append(time.perf_counter() - t0)
         if time.perf_counter() - t_all > budget_s:
             break
-    per_sweep = statistics.median(times)
-    return per_sweep, m.num_elements, len(times), name
+    per_tet = statistics.median(times) / m.num_elements
+    per_sweep = per_tet * m_full.num_elements
+    desc = (f"oracle port: {len(times)} sweeps of {name} ({m.num_elements} tets, injected precompute), "
+            f"median s/sweep scaled linearly by element count to {m_full.num_elements} tets")
+    if m_full.barrier is not None and len(m_full.surface_tris):
+        mc, stc, _, _ = scenes.build("c4s6")
+        t0 = time.perf_counter()
+        orc.find_pairs(mc, stc.x)
+        t_fp = time.perf_counter() - t0
+        scale = (len(m_full.surface_vertices) * len(m_full.surface_tris)) / (
+            len(mc.surface_vertices) * len(mc.surface_tris))
+        per_sweep += 3 * t_fp * scale
+        desc += (f" + 3 brute-force find_pairs per sweep: one call on c4s6 ({len(mc.surface_vertices)} sv x "
+                 f"{len(mc.surface_tris)} st) took {t_fp:.2f} s, scaled by n_sv*n_st x{scale:.0f} "
+                 f"(extrapolation; the reference cannot run C4's proximity arrays)")
+    return per_sweep, desc
+
+
+def traffic(config, kernel, launches, steps):
+    """DRAM bytes per launch of the roofline kernel from the committed ncu
+    capture (profiles/r1_traffic_<config>.json, dram__bytes_read.sum +
+    dram__bytes_write.sum summed over the kernel's launches in one sweep),
+    or None when no capture exists for this config."""
+    try:
+        t = json.loads((ROOT / "profiles" / f"r1_traffic_{config}.json").read_text())
+        if t.get("phase") != kernel or not launches:
+            return None
+        return t["dram_bytes_per_sweep"] / (launches / steps)
+    except Exception:
+        return None
 
 
 def threads():
@@ -150,7 +188,9 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--config", default=os.environ.get("JGS2_BENCH_CONFIG", "c3"))
+    # C4 (3.5M tets, ten puffer balls, IPC) is the configuration BASELINE.json's
+    # metric is quoted on; C3 (1M-tet twist, no contact) is the elastic-only case
+    ap.add_argument("--config", default=os.environ.get("JGS2_BENCH_CONFIG", "c4"))
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -163,19 +203,17 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        per, ne_s, n, name = cpu_sample(args.config, steps=max(args.steps, 1))
+        per, sample = cpu_sample(args.config, steps=max(min(args.steps, 3), 1))
         m_full, _, _, desc = scenes.build(args.config)
-        v = 1.0 / (per * m_full.num_elements / ne_s)
+        v = 1.0 / per
         cores = threads()
         line = {"impl": "reference", "metric": metric, "value": v, "unit": "sweeps/s",
-                "n_gpus": args.gpus, "steps": n, "warmup": 0,
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": 0,
                 "ms_per_step": 1e3 / v, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": desc, "parallelism": "1 CPU process"},
                 "cpu_baseline": {"value": v, "unit": "sweeps/s", "cores": cores, "kind": "port",
-                                 "sample": f"oracle port on {name} ({ne_s} tets, injected "
-                                           f"precompute), {n} sweeps, median s/sweep scaled "
-                                           f"linearly by element count to {m_full.num_elements}"},
+                                 "sample": sample},
                 "e2e": {"value": v, "unit": "sweeps/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
@@ -263,12 +301,9 @@ def main():
     cpu = None
     if rank == 0 and not args.no_cpu:
         try:
-            per, ne_s, n, name = cpu_sample(args.config)
-            v = 1.0 / (per * m.num_elements / ne_s)
-            cpu = {"value": v, "unit": "sweeps/s", "cores": threads(), "kind": "port",
-                   "sample": f"oracle port on {name} ({ne_s} tets, injected precompute), {n} "
-                             f"sweeps, median s/sweep scaled linearly by element count to "
-                             f"{m.num_elements} tets"}
+            per, sample = cpu_sample(args.config)
+            cpu = {"value": 1.0 / per, "unit": "sweeps/s", "cores": threads(), "kind": "port",
+                   "sample": sample}
         except Exception as exc:  # never fail the GPU line on the CPU sample
             cpu = {"value": None, "unit": "sweeps/s", "cores": threads(), "kind": "port",
                    "sample": f"failed: {exc}"}
@@ -295,10 +330,13 @@ def main():
         "roofline": {"bound": "hbm", "kernel": dom,
                      "dominant_phase": max(phases, key=lambda p: phases[p][0]), "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic(args.config, dom, d_launch, args.steps),
+                     "bytes_per_launch": d_bytes / max(d_launch, 1), "launches": d_launch,
                      "step_bytes": total_bytes / args.steps,
                      "step_frac": (total_bytes / (ms / 1e3) / 1e9) / peak},
         "phases_ms_per_step": {p: round(v[0] / args.steps, 4) for p, v in phases.items()},
+        "phases_gbs": {p: round(v[2] / (v[0] / 1e3) / 1e9, 1) for p, v in phases.items()
+                       if v[0] > 0 and v[2] > 0},
         "e2e": {"value": e2e, "unit": "sweeps/s", "h2d_bytes_per_step": 2 * 24 * nv,
                 "d2h_bytes_per_step": 2 * 24 * nv, "sweeps": e2e_sweeps,
                 "timing": "wall clock incl. host frame driver (compute_z, velocity update)"},

@@ -135,7 +135,8 @@ __device__ void sym_eig9_shared(double* V, double* d, double* e) {
       EE(i) = DD(i - 1);
       for (int j = 0; j < i; ++j) { DD(j) = VV(i - 1, j); VV(i, j) = 0.0; VV(j, i) = 0.0; }
     } else {
-      for (int k = 0; k < i; ++k) { DD(k) /= scale; h += DD(k) * DD(k); }
+      const double rs = 1.0 / scale;
+      for (int k = 0; k < i; ++k) { DD(k) *= rs; h += DD(k) * DD(k); }
       double f = DD(i - 1);
       double g = sqrt(h);
       if (f > 0) g = -g;
@@ -151,7 +152,8 @@ __device__ void sym_eig9_shared(double* V, double* d, double* e) {
         EE(j) = g;
       }
       f = 0.0;
-      for (int j = 0; j < i; ++j) { EE(j) /= h; f += EE(j) * DD(j); }
+      const double rh = 1.0 / h;
+      for (int j = 0; j < i; ++j) { EE(j) *= rh; f += EE(j) * DD(j); }
       double hh = f / (h + h);
       for (int j = 0; j < i; ++j) EE(j) -= hh * DD(j);
       for (int j = 0; j < i; ++j) {
@@ -169,7 +171,8 @@ __device__ void sym_eig9_shared(double* V, double* d, double* e) {
     VV(i, i) = 1.0;
     double h = DD(i + 1);
     if (h != 0.0) {
-      for (int k = 0; k <= i; ++k) DD(k) = VV(k, i + 1) / h;
+      const double rh = 1.0 / h;
+      for (int k = 0; k <= i; ++k) DD(k) = VV(k, i + 1) * rh;
       for (int j = 0; j <= i; ++j) {
         double g = 0.0;
         for (int k = 0; k <= i; ++k) g += VV(k, i + 1) * VV(k, j);
@@ -200,7 +203,7 @@ __device__ void sym_eig9_shared(double* V, double* d, double* e) {
         ++iter;
         double g = DD(l);
         double p = (DD(l + 1) - g) / (2.0 * EE(l));
-        double r = hypot(p, 1.0);
+        double r = sqrt(fma(p, p, 1.0));  // |p| <= ~1/eps: no overflow
         if (p < 0) r = -r;
         DD(l) = EE(l) / (p + r);
         DD(l + 1) = EE(l) * (p + r);
@@ -218,10 +221,12 @@ __device__ void sym_eig9_shared(double* V, double* d, double* e) {
           s2 = s;
           g = c * EE(i);
           h = c * p;
-          r = hypot(p, EE(i));
+          double ei = EE(i);
+          r = sqrt(fma(p, p, ei * ei));  // Hessian-scale entries: no overflow in FP64
           EE(i + 1) = s * r;
-          s = EE(i) / r;
-          c = p / r;
+          double ri = 1.0 / r;
+          s = ei * ri;
+          c = p * ri;
           p = c * DD(i) - s * g;
           DD(i + 1) = h + s * (c * g + s * DD(i));
           for (int k = 0; k < n; ++k) {

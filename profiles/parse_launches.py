@@ -26,6 +26,6 @@ if __name__ == "__main__":
         t[1] += it.get("gpu__time_duration.sum", 0) / 1e3
         t[2] += (it.get("dram__bytes_read.sum", 0) + it.get("dram__bytes_write.sum", 0)) / 1e6
     allt = sum(v[1] for v in tot.values())
-    print(f"{'kernel':28s} {'launches':>8s} {'total_us':>10s} {'share':>6s} {'MB':>10s} {'GB/s':>8s}")
+    print(f"{'kernel':28s} {'launches':>8s} {'total_us':>10s} {'share':>6s} {'MB':>10s} {'TB/s':>8s}")
     for k, (n, us, mb) in sorted(tot.items(), key=lambda kv: -kv[1][1]):
         print(f"{k[:28]:28s} {n:8d} {us:10.1f} {us / allt:6.1%} {mb:10.1f} {mb / us * 1e3 / 1e3 if us else 0:8.1f}")
