@@ -78,35 +78,6 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(rows)}
 
 
-def dist_setup():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    dist = None
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
-    return world, rank, local, dist
-
-
-def barrier(dist):
-    if dist is not None:
-        import torch
-        dist.barrier()
-        torch.cuda.synchronize()
-
-
-def max_over_ranks(dist, v):
-    if dist is None:
-        return v
-    import torch
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
-
-
 # ----------------------------------------------------------------- CPU oracle
 def cpu_sample(config, steps=3, budget_s=25.0):
     """Time the CPU oracle port (oracle/jgs2_oracle.py) on a bounded sample
@@ -194,7 +165,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
-    world, rank, local, dist = dist_setup()
+    from paper_2506_06494_b200 import replicas
+    world, rank, local, dist = replicas.setup()
+    barrier, max_over_ranks = replicas.barrier, replicas.max_over_ranks
     from paper_2506_06494_b200 import build as _build
     _build.build()  # no-op unless a CUDA source is newer than lib/libjgs2.so
     metric = "JGS2 iterations/sec (sweeps/s) and ms per timestep to residual tol"
@@ -245,12 +218,13 @@ def main():
     solver.timer_start()
     frames_done = solver.run_sweeps(args.steps, episode)
     ms = solver.timer_stop()
+    barrier(dist)
     clk = clocks.stop()
     launches = solver.kernel_launches - launches0
     ms = max_over_ranks(dist, ms)
     phases = solver.phase_stats()
     solver.profile(False)
-    value = world * args.steps / (ms / 1e3)
+    value = replicas.job_throughput(dist, args.steps, ms / 1e3)
 
     # roofline of the dominant HBM-modelled kernel (3x3-block arithmetic +
     # sparse triangular solves; the contact phases are latency/search bound
@@ -295,8 +269,7 @@ def main():
             if inf.dx_norm < cfg.tol_dx or e2e_sweeps >= args.e2e_steps:
                 break
         step_velocity_update(m, hs, xin.copy())
-    e2e_s = max_over_ranks(dist, time.perf_counter() - t_e2e)
-    e2e = world * e2e_sweeps / e2e_s
+    e2e = replicas.job_throughput(dist, e2e_sweeps, time.perf_counter() - t_e2e)
 
     cpu = None
     if rank == 0 and not args.no_cpu:
