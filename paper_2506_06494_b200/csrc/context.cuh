@@ -60,9 +60,10 @@ struct TriGrid {
 struct HierList {
   long long cap = 0, n = 0;
   long long *cnt = nullptr, *off = nullptr;
-  unsigned long long *ka = nullptr, *kb = nullptr;
+  unsigned *ka = nullptr, *kb = nullptr;  // dense cell index (all levels)
   int *ia = nullptr, *ib = nullptr;
-  int *over = nullptr, *n_over = nullptr;
+  int *cstart = nullptr, *cend = nullptr; // per-cell entry range [cstart, cend)
+  long long ncells_cap = 0;
 };
 
 // Device-side factor of the free-vertex rest Hessian (supernodal, ND order).
@@ -220,6 +221,8 @@ struct Ctx {
   int* hier_vlev = nullptr;
   int* hier_tlev = nullptr;
   unsigned* hier_masks = nullptr;
+  double* bbox_part = nullptr;  // surface bounding-box reduction (hier_grid.cuh)
+  double* bbox_res = nullptr;
   int* cand_v = nullptr;       // trial candidate pairs (vertex, triangle)
   int* cand_t = nullptr;
   int64_t cand_cap = 0;

@@ -248,6 +248,163 @@ __device__ void sym_eig9_shared(double* V, double* d, double* e) {
 #undef EE
 }
 
+// The same tred2 + tql2 (JAMA) with every loop bound a compile-time
+// constant (outer indices unrolled, runtime ranges as predicates), so the
+// diagonal d and off-diagonal e live in registers and only the eigenvector
+// matrix V stays in per-thread interleaved shared memory.
+template <int S>
+__device__ __forceinline__ void sym_eig9_reg(double* V, double (&d)[9], double (&e)[9]) {
+  constexpr int n = 9;
+#define VV(i, j) V[((i) * n + (j)) * S]
+#pragma unroll
+  for (int j = 0; j < n; ++j) d[j] = VV(n - 1, j);
+#pragma unroll
+  for (int i = n - 1; i > 0; --i) {
+    double scale = 0.0, h = 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k) scale += fabs(d[k]);
+    if (scale == 0.0) {
+      e[i] = d[i - 1];
+#pragma unroll
+      for (int j = 0; j < i; ++j) { d[j] = VV(i - 1, j); VV(i, j) = 0.0; VV(j, i) = 0.0; }
+    } else {
+      const double rs = 1.0 / scale;
+#pragma unroll
+      for (int k = 0; k < i; ++k) { d[k] *= rs; h += d[k] * d[k]; }
+      double f = d[i - 1];
+      double g = sqrt(h);
+      if (f > 0) g = -g;
+      e[i] = scale * g;
+      h -= f * g;
+      d[i - 1] = f - g;
+#pragma unroll
+      for (int j = 0; j < i; ++j) e[j] = 0.0;
+#pragma unroll
+      for (int j = 0; j < i; ++j) {
+        f = d[j];
+        VV(j, i) = f;
+        g = e[j] + VV(j, j) * f;
+#pragma unroll
+        for (int k = j + 1; k <= i - 1; ++k) {
+          double vkj = VV(k, j);
+          g += vkj * d[k];
+          e[k] += vkj * f;
+        }
+        e[j] = g;
+      }
+      f = 0.0;
+      const double rh = 1.0 / h;
+#pragma unroll
+      for (int j = 0; j < i; ++j) { e[j] *= rh; f += e[j] * d[j]; }
+      double hh = f / (h + h);
+#pragma unroll
+      for (int j = 0; j < i; ++j) e[j] -= hh * d[j];
+#pragma unroll
+      for (int j = 0; j < i; ++j) {
+        f = d[j];
+        g = e[j];
+#pragma unroll
+        for (int k = j; k <= i - 1; ++k) VV(k, j) -= (f * e[k] + g * d[k]);
+        d[j] = VV(i - 1, j);
+        VV(i, j) = 0.0;
+      }
+    }
+    d[i] = h;
+  }
+#pragma unroll
+  for (int i = 0; i < n - 1; ++i) {
+    VV(n - 1, i) = VV(i, i);
+    VV(i, i) = 1.0;
+    double h = d[i + 1];
+    if (h != 0.0) {
+      const double rh = 1.0 / h;
+#pragma unroll
+      for (int k = 0; k <= i; ++k) d[k] = VV(k, i + 1) * rh;
+#pragma unroll
+      for (int j = 0; j <= i; ++j) {
+        double g = 0.0;
+#pragma unroll
+        for (int k = 0; k <= i; ++k) g += VV(k, i + 1) * VV(k, j);
+#pragma unroll
+        for (int k = 0; k <= i; ++k) VV(k, j) -= g * d[k];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k <= i; ++k) VV(k, i + 1) = 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < n; ++j) { d[j] = VV(n - 1, j); VV(n - 1, j) = 0.0; }
+  VV(n - 1, n - 1) = 1.0;
+  // implicit QL
+#pragma unroll
+  for (int i = 1; i < n; ++i) e[i - 1] = e[i];
+  e[n - 1] = 0.0;
+  double f = 0.0, tst1 = 0.0;
+  const double eps = 2.220446049250313e-16;
+#pragma unroll
+  for (int l = 0; l < n; ++l) {
+    tst1 = fmax(tst1, fabs(d[l]) + fabs(e[l]));
+    int m = n - 1;  // first m >= l with |e[m]| <= eps tst1 (e[n-1] == 0)
+#pragma unroll
+    for (int mm = n - 2; mm >= l; --mm)
+      if (fabs(e[mm]) <= eps * tst1) m = mm;
+    if (l < n - 1 && m > l) {
+      int iter = 0;
+      do {
+        ++iter;
+        double g = d[l];
+        double p = (d[l + 1] - g) / (2.0 * e[l]);
+        double r = sqrt(fma(p, p, 1.0));  // |p| <= ~1/eps: no overflow
+        if (p < 0) r = -r;
+        d[l] = e[l] / (p + r);
+        d[l + 1] = e[l] * (p + r);
+        double dl1 = d[l + 1];
+        double h = g - d[l];
+#pragma unroll
+        for (int i = l + 2; i < n; ++i) d[i] -= h;
+        f += h;
+        p = d[n - 1];
+#pragma unroll
+        for (int i = n - 2; i > l; --i)
+          if (i == m) p = d[i];
+        double c = 1.0, c2 = c, c3 = c;
+        double el1 = e[l + 1];
+        double s = 0.0, s2 = 0.0;
+#pragma unroll
+        for (int i = n - 2; i >= l; --i) {
+          if (i < m) {
+            c3 = c2;
+            c2 = c;
+            s2 = s;
+            g = c * e[i];
+            h = c * p;
+            double ei = e[i];
+            r = sqrt(fma(p, p, ei * ei));  // Hessian-scale entries: no overflow in FP64
+            e[i + 1] = s * r;
+            double ri = 1.0 / r;
+            s = ei * ri;
+            c = p * ri;
+            p = c * d[i] - s * g;
+            d[i + 1] = h + s * (c * g + s * d[i]);
+#pragma unroll
+            for (int k = 0; k < n; ++k) {
+              double vk1 = VV(k, i + 1), vk0 = VV(k, i);
+              VV(k, i + 1) = s * vk0 + c * vk1;
+              VV(k, i) = c * vk0 - s * vk1;
+            }
+          }
+        }
+        p = -s * s2 * c3 * el1 * e[l] / dl1;
+        e[l] = s * p;
+        d[l] = c * p;
+      } while (fabs(e[l]) > eps * tst1 && iter < 60);
+    }
+    d[l] = d[l] + f;
+    e[l] = 0.0;
+  }
+#undef VV
+}
+
 // One thread per element: closed-form M, LDL^T inertia test, and (when
 // indefinite) the tred2/tql2 projection on per-thread interleaved shared
 // memory. The number of indefinite elements is accumulated with one
@@ -285,8 +442,6 @@ k_element_mplus(int n, const int* elems, const double* __restrict__ xs, const in
     } else {
       indef = true;
       double* Vs = hsm + threadIdx.x;
-      double* ds = hsm + 81 * kHessThreads + threadIdx.x;
-      double* es = hsm + 90 * kHessThreads + threadIdx.x;
 #pragma unroll
       for (int i = 0; i < 9; ++i)
 #pragma unroll
@@ -294,24 +449,30 @@ k_element_mplus(int n, const int* elems, const double* __restrict__ xs, const in
           Vs[(9 * i + j) * kHessThreads] = Mp[JGS2_PK(i, j)];
           Vs[(9 * j + i) * kHessThreads] = Mp[JGS2_PK(i, j)];
         }
-      sym_eig9_shared<kHessThreads>(Vs, ds, es);
+      double dg[9], od[9];
+      sym_eig9_reg<kHessThreads>(Vs, dg, od);
       double lam[9];
 #pragma unroll
-      for (int q = 0; q < 9; ++q) lam[q] = fmax(ds[q * kHessThreads], 0.0);
-      for (int i = 0; i < 9; ++i)
+      for (int q = 0; q < 9; ++q) lam[q] = fmax(dg[q], 0.0);
+#pragma unroll
+      for (int i = 0; i < 9; ++i) {
+        double vi[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) vi[q] = Vs[(9 * i + q) * kHessThreads] * lam[q];
+#pragma unroll
         for (int j = 0; j <= i; ++j) {
           double acc = 0.0;
 #pragma unroll
-          for (int q = 0; q < 9; ++q)
-            acc += Vs[(9 * i + q) * kHessThreads] * lam[q] * Vs[(9 * j + q) * kHessThreads];
+          for (int q = 0; q < 9; ++q) acc += vi[q] * Vs[(9 * j + q) * kHessThreads];
           o[JGS2_PK(i, j)] = acc;
         }
+      }
     }
   }
   unsigned ball = __ballot_sync(0xffffffffu, indef);
   if ((threadIdx.x & 31) == 0 && ball) atomicAdd(count, __popc(ball));
 }
-constexpr size_t kHessSmemBytes = 99 * kHessThreads * sizeof(double);
+constexpr size_t kHessSmemBytes = 81 * kHessThreads * sizeof(double);
 
 // count: device int, zeroed here; list: unused (kept for the call sites).
 inline void launch_element_mplus(int n, const int* elems, const double* xs, const int4* tets,

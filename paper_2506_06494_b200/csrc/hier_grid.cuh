@@ -35,6 +35,14 @@
 //     boxes (a cell both objects cover).
 // Cell entries are in ascending object order and objects are numbered body
 // by body, so own-body runs are skipped without being read (own_run).
+//
+// Cells are indexed densely: every level's grid covers the bounding box of
+// the surface (cell coordinates are clamped to it, which keeps every
+// overlapping pair of boxes meeting: an overlap of two boxes around objects
+// inside the bounding box always reaches into it), a 32-bit key is the
+// level's offset plus the row-major cell index, and a per-cell [start, end)
+// directory built after the radix sort replaces a binary search per lookup.
+// The level-0 cell is at least 1/255 of the largest extent.
 #pragma once
 #include <chrono>
 #include "broadphase.cuh"
@@ -48,6 +56,13 @@ constexpr int kHierBig = 0x100;  // level flag: object scans all opposing object
 
 enum HierMode { HIER_MIN = 0, HIER_COUNT = 1, HIER_WRITE = 2 };
 
+struct HierGeom {
+  double org[3];              // bounding-box origin (lower corner)
+  int n[kHierLevels][3];      // cells per axis at each level
+  unsigned off[kHierLevels];  // first cell index of each level
+  unsigned ncells;            // all levels
+};
+
 struct HierArgs {
   ContactDev cd;
   const double* x;
@@ -56,6 +71,8 @@ struct HierArgs {
   double pad;    // radius added to every object
   double cell;   // level-0 cell size
   double dlim;   // LIST mode: keep pairs with dist < 2 pad + b (s_v + s_t) (slack included in b, pad)
+  HierGeom g;
+  unsigned long long* stats = nullptr;  // diagnostics (JGS2_DEBUG_HIER): cells, cross entries, pairs
 };
 
 __device__ __forceinline__ int hier_level(double rho, double cell) {
@@ -64,11 +81,14 @@ __device__ __forceinline__ int hier_level(double rho, double cell) {
   if (!(q < kHierLevels - 1)) return kHierLevels - 1;  // also catches NaN
   return q < 0 ? 0 : (int)q;
 }
-__device__ __forceinline__ unsigned long long hier_key(int level, long long ix, long long iy, long long iz) {
-  const long long off = 1LL << 19;
-  auto cl = [&](long long c) { return c < -off + 1 ? -off + 1 : (c > off - 2 ? off - 2 : c); };
-  return ((unsigned long long)level << 60) | ((unsigned long long)(cl(ix) + off) << 40) |
-         ((unsigned long long)(cl(iy) + off) << 20) | (unsigned long long)(cl(iz) + off);
+// clamped cell coordinate along axis k at level L (monotone in v)
+__device__ __forceinline__ int hier_coord(const HierArgs& a, int L, int k, double v, double inv) {
+  double c = floor((v - a.g.org[k]) * inv);
+  int hi = a.g.n[L][k] - 1;
+  return c < 0.0 ? 0 : (c > (double)hi ? hi : (int)c);  // NaN -> hi
+}
+__device__ __forceinline__ unsigned hier_cell(const HierArgs& a, int L, int i, int j, int k) {
+  return a.g.off[L] + ((unsigned)k * a.g.n[L][1] + j) * a.g.n[L][0] + i;
 }
 
 __device__ __forceinline__ double tri_step(const double* dx, const int* st, int t) {
@@ -89,32 +109,32 @@ __device__ __forceinline__ void vtx_box(const HierArgs& a, int v, double r, doub
 __device__ __forceinline__ double vtx_rho(const HierArgs& a, int v) { return a.b * norm3_np(a.dx + 3 * v) + a.pad; }
 __device__ __forceinline__ double tri_rho(const HierArgs& a, int t) { return a.b * tri_step(a.dx, a.cd.st, t) + a.pad; }
 
-__device__ __forceinline__ long long box_cells(const double* lo, const double* hi, double inv, long long* c0,
-                                               long long* c1) {
+__device__ __forceinline__ double level_inv(const HierArgs& a, int L) { return 1.0 / (a.cell * (double)(1LL << L)); }
+
+// clamped cell range of a box at level L; returns the number of cells
+__device__ __forceinline__ long long box_cells(const HierArgs& a, int L, const double* lo, const double* hi,
+                                               int* c0, int* c1) {
+  double inv = level_inv(a, L);
   long long n = 1;
   for (int k = 0; k < 3; ++k) {
-    c0[k] = (long long)floor(lo[k] * inv);
-    c1[k] = (long long)floor(hi[k] * inv);
-    long long w = c1[k] - c0[k] + 1;
-    if (!(w > 0) || w > kHierMaxCells) return kHierMaxCells + 1;
-    n *= w;
-    if (n > kHierMaxCells) return kHierMaxCells + 1;
+    c0[k] = hier_coord(a, L, k, lo[k], inv);
+    c1[k] = hier_coord(a, L, k, hi[k], inv);
+    n *= (long long)(c1[k] - c0[k] + 1);
   }
   return n;
 }
-__device__ __forceinline__ double level_inv(const HierArgs& a, int L) { return 1.0 / (a.cell * (double)(1LL << L)); }
 
 // per-object levels (+ kHierBig) and level occupancy masks
 __global__ void k_hier_levels(HierArgs a, int* vlev, int* tlev, unsigned* vmask, unsigned* tmask) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   double lo[3], hi[3];
-  long long c0[3], c1[3];
+  int c0[3], c1[3];
   if (i < a.cd.nsv) {
     int v = a.cd.sv[i];
     double r = vtx_rho(a, v);
     int l = hier_level(r, a.cell);
     vtx_box(a, v, r, lo, hi);
-    bool big = box_cells(lo, hi, level_inv(a, l), c0, c1) > kHierMaxCells;
+    bool big = box_cells(a, l, lo, hi, c0, c1) > kHierMaxCells;
     vlev[i] = l | (big ? kHierBig : 0);
     atomicOr(vmask, 1u << l);
   }
@@ -122,7 +142,7 @@ __global__ void k_hier_levels(HierArgs a, int* vlev, int* tlev, unsigned* vmask,
     double r = tri_rho(a, i);
     int l = hier_level(r, a.cell);
     tri_box(a, i, r, lo, hi);
-    bool big = box_cells(lo, hi, level_inv(a, l), c0, c1) > kHierMaxCells;
+    bool big = box_cells(a, l, lo, hi, c0, c1) > kHierMaxCells;
     tlev[i] = l | (big ? kHierBig : 0);
     atomicOr(tmask, 1u << l);
   }
@@ -132,19 +152,18 @@ __global__ void k_hier_levels(HierArgs a, int* vlev, int* tlev, unsigned* vmask,
 // level that the opposing side occupies (big objects: none)
 template <bool WRITE>
 __device__ __forceinline__ long long hier_entries(const HierArgs& a, const double* lo, const double* hi, int lev,
-                                                  unsigned mask, int id, unsigned long long* keys, int* ids,
-                                                  long long o) {
+                                                  unsigned mask, int id, unsigned* keys, int* ids, long long o) {
   if (lev & kHierBig) return 0;
   long long n = 0;
   for (int L = lev; L < kHierLevels; ++L) {
     if (!((mask >> L) & 1u)) continue;
-    long long c0[3], c1[3];
-    long long nc = box_cells(lo, hi, level_inv(a, L), c0, c1);
+    int c0[3], c1[3];
+    long long nc = box_cells(a, L, lo, hi, c0, c1);
     if (WRITE)
-      for (long long i = c0[0]; i <= c1[0]; ++i)
-        for (long long j = c0[1]; j <= c1[1]; ++j)
-          for (long long k = c0[2]; k <= c1[2]; ++k) {
-            keys[o] = hier_key(L, i, j, k);
+      for (int k = c0[2]; k <= c1[2]; ++k)
+        for (int j = c0[1]; j <= c1[1]; ++j)
+          for (int i = c0[0]; i <= c1[0]; ++i) {
+            keys[o] = hier_cell(a, L, i, j, k);
             ids[o] = id;
             ++o;
           }
@@ -155,7 +174,7 @@ __device__ __forceinline__ long long hier_entries(const HierArgs& a, const doubl
 
 template <bool WRITE>
 __global__ void k_hier_tri_entries(HierArgs a, const int* tlev, const unsigned* vmask, const long long* off,
-                                   long long* cnt, unsigned long long* keys, int* ids) {
+                                   long long* cnt, unsigned* keys, int* ids) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= a.cd.nst) return;
   double lo[3], hi[3];
@@ -166,7 +185,7 @@ __global__ void k_hier_tri_entries(HierArgs a, const int* tlev, const unsigned* 
 
 template <bool WRITE>
 __global__ void k_hier_vtx_entries(HierArgs a, const int* vlev, const unsigned* tmask, const long long* off,
-                                   long long* cnt, unsigned long long* keys, int* ids) {
+                                   long long* cnt, unsigned* keys, int* ids) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.cd.nsv) return;
   double lo[3], hi[3];
@@ -175,14 +194,13 @@ __global__ void k_hier_vtx_entries(HierArgs a, const int* vlev, const unsigned* 
   if (!WRITE) cnt[i] = n;
 }
 
-__device__ __forceinline__ void key_range(const unsigned long long* keys, long long n, unsigned long long key,
-                                          long long* first, long long* last) {
-  long long lo = 0, hi = n;
-  while (lo < hi) { long long m = (lo + hi) >> 1; if (keys[m] < key) lo = m + 1; else hi = m; }
-  *first = lo;
-  hi = n;
-  while (lo < hi) { long long m = (lo + hi) >> 1; if (keys[m] <= key) lo = m + 1; else hi = m; }
-  *last = lo;
+// per-cell [start, end) of the sorted entries (cells without entries keep 0, 0)
+__global__ void k_hier_dir(const unsigned* keys, long long n, int* cstart, int* cend) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned k = keys[i];
+  if (i == 0 || keys[i - 1] != k) cstart[k] = (int)i;
+  if (i == n - 1 || keys[i + 1] != k) cend[k] = (int)(i + 1);
 }
 
 // dist(x_v, T(x)) and the pair's step rate s_v + s_t (cross-body pairs only)
@@ -194,11 +212,11 @@ __device__ __forceinline__ double pair_dist(const HierArgs& a, int v, int t, dou
   return closest_point_tri(a.x + 3 * v, a.x + 3 * a0, a.x + 3 * a1, a.x + 3 * a2, bary);
 }
 
-// the min-corner cell rule: is (p, q, s) the cell of max(lo_a, lo_b)?
-__device__ __forceinline__ bool owns_pair(const double* la, const double* lb, double inv, long long p, long long q,
-                                          long long s) {
-  return (long long)floor(fmax(la[0], lb[0]) * inv) == p && (long long)floor(fmax(la[1], lb[1]) * inv) == q &&
-         (long long)floor(fmax(la[2], lb[2]) * inv) == s;
+// the min-corner cell rule: is (p, q, s) the (clamped) cell of max(lo_a, lo_b)?
+__device__ __forceinline__ bool owns_pair(const HierArgs& a, int L, const double* la, const double* lb, double inv,
+                                          int p, int q, int s) {
+  return hier_coord(a, L, 0, fmax(la[0], lb[0]), inv) == p && hier_coord(a, L, 1, fmax(la[1], lb[1]), inv) == q &&
+         hier_coord(a, L, 2, fmax(la[2], lb[2]), inv) == s;
 }
 
 struct HierOut {
@@ -207,8 +225,13 @@ struct HierOut {
   long long o = 0;        // WRITE cursor
   int* cv = nullptr;
   int* ct = nullptr;
+  unsigned long long ncell = 0, nent = 0, npair = 0;
+  __device__ __forceinline__ void flush(const HierArgs& a) {
+    if (a.stats) { atomicAdd(a.stats, ncell); atomicAdd(a.stats + 1, nent); atomicAdd(a.stats + 2, npair); }
+  }
   template <int MODE>
   __device__ __forceinline__ void take(const HierArgs& a, int v, int t) {
+    ++npair;
     double rate;
     double d = pair_dist(a, v, t, &rate);
     if (MODE == HIER_MIN) {
@@ -222,9 +245,9 @@ struct HierOut {
 
 // vertex-side queries: triangle grid at the vertex's level (big: all triangles)
 template <int MODE>
-__global__ void k_hier_query_v(HierArgs a, const int* vlev, const int* tlev, const unsigned long long* tkeys,
-                               const int* tids, long long ntk, const long long* off, long long* cnt, int* cv,
-                               int* ct, double* partials, unsigned* counter, double* out) {
+__global__ void k_hier_query_v(HierArgs a, const int* vlev, const int* tlev, const int* cstart, const int* cend,
+                               const int* tids, const long long* off, long long* cnt, int* cv, int* ct,
+                               double* partials, unsigned* counter, double* out) {
   HierOut R;
   R.cv = cv; R.ct = ct;
   int i0 = blockIdx.x * blockDim.x + threadIdx.x;
@@ -241,18 +264,20 @@ __global__ void k_hier_query_v(HierArgs a, const int* vlev, const int* tlev, con
       double lo[3], hi[3], tl[3], th[3];
       vtx_box(a, v, vtx_rho(a, v), lo, hi);
       double inv = level_inv(a, lev);
-      long long c0[3], c1[3];
-      box_cells(lo, hi, inv, c0, c1);
-      for (long long p = c0[0]; p <= c1[0]; ++p)
-        for (long long q = c0[1]; q <= c1[1]; ++q)
-          for (long long s = c0[2]; s <= c1[2]; ++s) {
-            long long f, l;
-            key_range(tkeys, ntk, hier_key(lev, p, q, s), &f, &l);
+      int c0[3], c1[3];
+      box_cells(a, lev, lo, hi, c0, c1);
+      for (int s = c0[2]; s <= c1[2]; ++s)
+        for (int q = c0[1]; q <= c1[1]; ++q)
+          for (int p = c0[0]; p <= c1[0]; ++p) {
+            unsigned cell = hier_cell(a, lev, p, q, s);
+            long long f = cstart[cell], l = cend[cell];
+            ++R.ncell;
             visit_cross(f, l, bv, [&](long long e) { return a.cd.tbody[tids[e]]; }, [&](long long e) {
+              ++R.nent;
               int t = tids[e];
               if (MODE != HIER_MIN) {
                 tri_box(a, t, tri_rho(a, t), tl, th);
-                if (!owns_pair(lo, tl, inv, p, q, s)) return;
+                if (!owns_pair(a, lev, lo, tl, inv, p, q, s)) return;
               }
               R.take<MODE>(a, v, t);
             });
@@ -260,14 +285,15 @@ __global__ void k_hier_query_v(HierArgs a, const int* vlev, const int* tlev, con
     }
     if (MODE == HIER_COUNT) cnt[i] = R.n, R.n = 0;
   }
+  R.flush(a);
   if (MODE == HIER_MIN) grid_reduce<OP_MIN>(R.mn, partials, counter, out);
 }
 
 // triangle-side queries: vertex grid at the triangle's level (big: all vertices)
 template <int MODE>
-__global__ void k_hier_query_t(HierArgs a, const int* vlev, const int* tlev, const unsigned long long* vkeys,
-                               const int* vids, long long nvk, const long long* off, long long* cnt, int* cv,
-                               int* ct, double* partials, unsigned* counter, double* out) {
+__global__ void k_hier_query_t(HierArgs a, const int* vlev, const int* tlev, const int* cstart, const int* cend,
+                               const int* vids, const long long* off, long long* cnt, int* cv, int* ct,
+                               double* partials, unsigned* counter, double* out) {
   HierOut R;
   R.cv = cv; R.ct = ct;
   int t0 = blockIdx.x * blockDim.x + threadIdx.x;
@@ -285,20 +311,22 @@ __global__ void k_hier_query_t(HierArgs a, const int* vlev, const int* tlev, con
       double lo[3], hi[3], vl[3], vh[3];
       tri_box(a, t, tri_rho(a, t), lo, hi);
       double inv = level_inv(a, lev);
-      long long c0[3], c1[3];
-      box_cells(lo, hi, inv, c0, c1);
-      for (long long p = c0[0]; p <= c1[0]; ++p)
-        for (long long q = c0[1]; q <= c1[1]; ++q)
-          for (long long s = c0[2]; s <= c1[2]; ++s) {
-            long long f, l;
-            key_range(vkeys, nvk, hier_key(lev, p, q, s), &f, &l);
+      int c0[3], c1[3];
+      box_cells(a, lev, lo, hi, c0, c1);
+      for (int s = c0[2]; s <= c1[2]; ++s)
+        for (int q = c0[1]; q <= c1[1]; ++q)
+          for (int p = c0[0]; p <= c1[0]; ++p) {
+            unsigned cell = hier_cell(a, lev, p, q, s);
+            long long f = cstart[cell], l = cend[cell];
+            ++R.ncell;
             visit_cross(f, l, bt, [&](long long e) { return a.cd.vbody[a.cd.sv[vids[e]]]; }, [&](long long e) {
+              ++R.nent;
               int i = vids[e];
               int v = a.cd.sv[i];
               if (MODE != HIER_MIN) {
                 if ((vlev[i] & ~kHierBig) >= lev) return;  // level tie: the vertex side has it
                 vtx_box(a, v, vtx_rho(a, v), vl, vh);
-                if (!owns_pair(lo, vl, inv, p, q, s)) return;
+                if (!owns_pair(a, lev, lo, vl, inv, p, q, s)) return;
               }
               R.take<MODE>(a, v, t);
             });
@@ -306,7 +334,68 @@ __global__ void k_hier_query_t(HierArgs a, const int* vlev, const int* tlev, con
     }
     if (MODE == HIER_COUNT) cnt[t] = R.n, R.n = 0;
   }
+  R.flush(a);
   if (MODE == HIER_MIN) grid_reduce<OP_MIN>(R.mn, partials, counter, out);
+}
+
+// bounding box of the surface vertices: per-block (min xyz, -max xyz), then one block
+__global__ void k_sv_bbox(ContactDev cd, const double* x, double* part) {
+  double m[6] = {INFINITY, INFINITY, INFINITY, INFINITY, INFINITY, INFINITY};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cd.nsv; i += gridDim.x * blockDim.x) {
+    const double* p = x + 3 * cd.sv[i];
+    for (int k = 0; k < 3; ++k) { m[k] = fmin(m[k], p[k]); m[3 + k] = fmin(m[3 + k], -p[k]); }
+  }
+  for (int k = 0; k < 6; ++k) {
+    double r = block_reduce<OP_MIN>(m[k]);
+    if (threadIdx.x == 0) part[k * kMaxPartials + blockIdx.x] = r;
+    __syncthreads();
+  }
+}
+__global__ void k_bbox_final(const double* part, int nb, double* out) {
+  for (int k = 0; k < 6; ++k) {
+    double m = INFINITY;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) m = fmin(m, part[k * kMaxPartials + i]);
+    m = block_reduce<OP_MIN>(m);
+    if (threadIdx.x == 0) out[k] = m;
+    __syncthreads();
+  }
+}
+
+// level-0 cell and the dense per-level grids over the surface's bounding box
+inline void hier_geometry(Ctx& C, const double* x, HierArgs& a) {
+  if (!C.bbox_part) {
+    C.bbox_part = C.alloc<double>(6 * kMaxPartials);
+    C.bbox_res = C.alloc<double>(6);
+  }
+  int nb = std::min(red_grid(C.nsv), kMaxPartials);
+  k_sv_bbox<<<nb, kBlock, 0, C.stream>>>(contactdev(C), x, C.bbox_part);
+  C.check_launch();
+  k_bbox_final<<<1, kBlock, 0, C.stream>>>(C.bbox_part, nb, C.bbox_res);
+  C.check_launch();
+  double bb[6];
+  JGS2_CUDA(cudaMemcpyAsync(bb, C.bbox_res, sizeof(bb), cudaMemcpyDeviceToHost, C.stream));
+  C.sync();
+  double ext[3], emax = 0.0;
+  for (int k = 0; k < 3; ++k) {
+    double lo = bb[k], hi = -bb[3 + k];
+    if (!std::isfinite(lo) || !std::isfinite(hi) || hi < lo) lo = hi = 0.0;  // clamping keeps any box correct
+    a.g.org[k] = lo;
+    ext[k] = hi - lo;
+    emax = std::max(emax, ext[k]);
+  }
+  a.cell = std::max(C.grid_cell, emax / 255.0);
+  unsigned off = 0;
+  for (int L = 0; L < kHierLevels; ++L) {
+    double cl = a.cell * (double)(1LL << L);
+    long long cells = 1;
+    for (int k = 0; k < 3; ++k) {
+      a.g.n[L][k] = (int)std::min(256.0, std::floor(ext[k] / cl) + 1.0);
+      cells *= a.g.n[L][k];
+    }
+    a.g.off[L] = off;
+    off += (unsigned)cells;
+  }
+  a.g.ncells = off;
 }
 
 inline void hier_alloc(Ctx& C, HierList& h, int nobj) {
@@ -330,8 +419,15 @@ inline long long scan_counts(Ctx& C, long long* cnt, long long* off, long long n
 }
 
 template <class CountK, class WriteK>
-inline void hier_build(Ctx& C, HierList& h, int nobj, CountK count, WriteK write) {
+inline void hier_build(Ctx& C, HierList& h, int nobj, unsigned ncells, CountK count, WriteK write) {
   hier_alloc(C, h, nobj);
+  if ((long long)ncells > h.ncells_cap) {
+    h.cstart = C.alloc<int>(ncells);
+    h.cend = C.alloc<int>(ncells);
+    h.ncells_cap = ncells;
+  }
+  JGS2_CUDA(cudaMemsetAsync(h.cstart, 0, ncells * sizeof(int), C.stream));
+  JGS2_CUDA(cudaMemsetAsync(h.cend, 0, ncells * sizeof(int), C.stream));
   count(h);
   C.check_launch();
   long long total = scan_counts(C, h.cnt, h.off, nobj);
@@ -339,7 +435,7 @@ inline void hier_build(Ctx& C, HierList& h, int nobj, CountK count, WriteK write
     throw Error(-2, "hierarchical grid: entry count " + std::to_string(total) + " out of range");
   if (total > h.cap) {
     long long cap = std::max<long long>(total + total / 2, 4096);
-    h.ka = C.alloc<unsigned long long>(cap); h.kb = C.alloc<unsigned long long>(cap);
+    h.ka = C.alloc<unsigned>(cap); h.kb = C.alloc<unsigned>(cap);
     h.ia = C.alloc<int>(cap); h.ib = C.alloc<int>(cap);
     h.cap = cap;
   }
@@ -347,16 +443,21 @@ inline void hier_build(Ctx& C, HierList& h, int nobj, CountK count, WriteK write
   if (total == 0) return;
   write(h);
   C.check_launch();
+  int bits = 1;
+  while (bits < 32 && (1ull << bits) < (unsigned long long)ncells) ++bits;
   size_t sb = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, sb, h.ka, h.kb, h.ia, h.ib, (int)total, 0, 64, C.stream);
+  cub::DeviceRadixSort::SortPairs(nullptr, sb, h.ka, h.kb, h.ia, h.ib, (int)total, 0, bits, C.stream);
   if (sb > C.scan_temp_bytes) { C.scan_temp = C.alloc<char>(sb); C.scan_temp_bytes = sb; }
-  JGS2_CUDA(cub::DeviceRadixSort::SortPairs(C.scan_temp, sb, h.ka, h.kb, h.ia, h.ib, (int)total, 0, 64,
+  JGS2_CUDA(cub::DeviceRadixSort::SortPairs(C.scan_temp, sb, h.ka, h.kb, h.ia, h.ib, (int)total, 0, bits,
                                             C.stream));
   ++C.launches;
+  k_hier_dir<<<grid_for(total), kBlock, 0, C.stream>>>(h.kb, total, h.cstart, h.cend);
+  C.check_launch();
 }
 
 // levels + both grids for radii b * s + pad
-inline void hier_prepare(Ctx& C, const HierArgs& a) {
+inline void hier_prepare(Ctx& C, HierArgs& a, const double* x) {
+  hier_geometry(C, x, a);
   if (!C.hier_vlev) {
     C.hier_vlev = C.alloc<int>(C.nsv + 1);
     C.hier_tlev = C.alloc<int>(C.nst + 1);
@@ -367,7 +468,7 @@ inline void hier_prepare(Ctx& C, const HierArgs& a) {
   k_hier_levels<<<grid_for(nmax), kBlock, 0, C.stream>>>(a, C.hier_vlev, C.hier_tlev, C.hier_masks,
                                                          C.hier_masks + 1);
   C.check_launch();
-  hier_build(C, C.hier_tri, C.nst,
+  hier_build(C, C.hier_tri, C.nst, a.g.ncells,
              [&](HierList& h) {
                k_hier_tri_entries<false><<<grid_for(C.nst), kBlock, 0, C.stream>>>(
                    a, C.hier_tlev, C.hier_masks, nullptr, h.cnt, nullptr, nullptr);
@@ -376,7 +477,7 @@ inline void hier_prepare(Ctx& C, const HierArgs& a) {
                k_hier_tri_entries<true><<<grid_for(C.nst), kBlock, 0, C.stream>>>(
                    a, C.hier_tlev, C.hier_masks, h.off, nullptr, h.ka, h.ia);
              });
-  hier_build(C, C.hier_vtx, C.nsv,
+  hier_build(C, C.hier_vtx, C.nsv, a.g.ncells,
              [&](HierList& h) {
                k_hier_vtx_entries<false><<<grid_for(C.nsv), kBlock, 0, C.stream>>>(
                    a, C.hier_vlev, C.hier_masks + 1, nullptr, h.cnt, nullptr, nullptr);
@@ -400,20 +501,26 @@ inline double hier_min_ratio(Ctx& C, const double* x, const double* dx, double b
   a.dlim = 0.0;
   bool dbg = getenv("JGS2_DEBUG_HIER") != nullptr;
   auto now = [&]() { if (dbg) C.sync(); return std::chrono::steady_clock::now(); };
+  unsigned long long* st = nullptr;
+  if (dbg) {
+    JGS2_CUDA(cudaMalloc(&st, 6 * sizeof(unsigned long long)));
+    JGS2_CUDA(cudaMemset(st, 0, 6 * sizeof(unsigned long long)));
+    a.stats = st;
+  }
   auto t0 = now();
-  hier_prepare(C, a);
+  hier_prepare(C, a, x);
   auto t1 = now();
   const HierList& T = C.hier_tri;
   const HierList& V = C.hier_vtx;
   double* part = C.partials + R_CAP * kMaxPartials;
   double m[2] = {INFINITY, INFINITY};
   k_hier_query_v<HIER_MIN><<<red_grid(C.nsv), kBlock, 0, C.stream>>>(
-      a, C.hier_vlev, C.hier_tlev, T.kb, T.ib, T.n, nullptr, nullptr, nullptr, nullptr, part,
+      a, C.hier_vlev, C.hier_tlev, T.cstart, T.cend, T.ib, nullptr, nullptr, nullptr, nullptr, part,
       C.counters + R_CAP, C.res + R_CAP);
   C.check_launch();
   JGS2_CUDA(cudaMemcpyAsync(&m[0], C.res + R_CAP, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
   k_hier_query_t<HIER_MIN><<<red_grid(C.nst), kBlock, 0, C.stream>>>(
-      a, C.hier_vlev, C.hier_tlev, V.kb, V.ib, V.n, nullptr, nullptr, nullptr, nullptr, part,
+      a, C.hier_vlev, C.hier_tlev, V.cstart, V.cend, V.ib, nullptr, nullptr, nullptr, nullptr, part,
       C.counters + R_CAP, C.res + R_CAP);
   C.check_launch();
   JGS2_CUDA(cudaMemcpyAsync(&m[1], C.res + R_CAP, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
@@ -423,8 +530,12 @@ inline double hier_min_ratio(Ctx& C, const double* x, const double* dx, double b
     unsigned mk[2];
     JGS2_CUDA(cudaMemcpy(mk, C.hier_masks, sizeof(mk), cudaMemcpyDeviceToHost));
     auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-    fprintf(stderr, "hier_min_ratio b=%.3e entries tri=%lld vtx=%lld masks v=%x t=%x m=%.3e %.3e ms prep %.2f q %.2f\n",
-            a.b, T.n, V.n, mk[0], mk[1], m[0], m[1], ms(t0, t1), ms(t1, t2));
+    unsigned long long hs[3];
+    JGS2_CUDA(cudaMemcpy(hs, st, sizeof(hs), cudaMemcpyDeviceToHost));
+    cudaFree(st);
+    fprintf(stderr, "hier_min_ratio b=%.3e cell=%.3e ncells=%u entries tri=%lld vtx=%lld masks v=%x t=%x m=%.3e %.3e "
+            "ms prep %.2f q %.2f | cells %llu cross %llu pairs %llu\n",
+            a.b, a.cell, a.g.ncells, T.n, V.n, mk[0], mk[1], m[0], m[1], ms(t0, t1), ms(t1, t2), hs[0], hs[1], hs[2]);
   }
   return std::fmin(m[0], m[1]);
 }
@@ -466,7 +577,7 @@ inline long long hier_candidates(Ctx& C, const double* x, const double* dx, doub
   a.pad = 0.5 * C.dhat * (1.0 + 1e-6);
   a.cell = C.grid_cell;
   a.dlim = 2.0 * a.pad;
-  hier_prepare(C, a);
+  hier_prepare(C, a, x);
   const HierList& T = C.hier_tri;
   const HierList& V = C.hier_vtx;
   long long nobj = (long long)C.nsv + C.nst;
@@ -477,11 +588,11 @@ inline long long hier_candidates(Ctx& C, const double* x, const double* dx, doub
   long long* cv_cnt = C.cand_cnt;
   long long* ct_cnt = C.cand_cnt + C.nsv;
   k_hier_query_v<HIER_COUNT><<<grid_for(C.nsv), kBlock, 0, C.stream>>>(
-      a, C.hier_vlev, C.hier_tlev, T.kb, T.ib, T.n, nullptr, cv_cnt, nullptr, nullptr, nullptr, nullptr,
+      a, C.hier_vlev, C.hier_tlev, T.cstart, T.cend, T.ib, nullptr, cv_cnt, nullptr, nullptr, nullptr, nullptr,
       nullptr);
   C.check_launch();
   k_hier_query_t<HIER_COUNT><<<grid_for(C.nst), kBlock, 0, C.stream>>>(
-      a, C.hier_vlev, C.hier_tlev, V.kb, V.ib, V.n, nullptr, ct_cnt, nullptr, nullptr, nullptr, nullptr,
+      a, C.hier_vlev, C.hier_tlev, V.cstart, V.cend, V.ib, nullptr, ct_cnt, nullptr, nullptr, nullptr, nullptr,
       nullptr);
   C.check_launch();
   long long total = scan_counts(C, C.cand_cnt, C.cand_off, nobj);
@@ -494,11 +605,11 @@ inline long long hier_candidates(Ctx& C, const double* x, const double* dx, doub
   }
   if (total == 0) return 0;
   k_hier_query_v<HIER_WRITE><<<grid_for(C.nsv), kBlock, 0, C.stream>>>(
-      a, C.hier_vlev, C.hier_tlev, T.kb, T.ib, T.n, C.cand_off, nullptr, C.cand_v, C.cand_t, nullptr,
+      a, C.hier_vlev, C.hier_tlev, T.cstart, T.cend, T.ib, C.cand_off, nullptr, C.cand_v, C.cand_t, nullptr,
       nullptr, nullptr);
   C.check_launch();
   k_hier_query_t<HIER_WRITE><<<grid_for(C.nst), kBlock, 0, C.stream>>>(
-      a, C.hier_vlev, C.hier_tlev, V.kb, V.ib, V.n, C.cand_off + C.nsv, nullptr, C.cand_v, C.cand_t,
+      a, C.hier_vlev, C.hier_tlev, V.cstart, V.cend, V.ib, C.cand_off + C.nsv, nullptr, C.cand_v, C.cand_t,
       nullptr, nullptr, nullptr);
   C.check_launch();
   return total;
