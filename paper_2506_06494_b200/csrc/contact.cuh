@@ -12,6 +12,7 @@
 #include "sweep.cuh"
 #include "geometry.cuh"
 #include "broadphase.cuh"
+#include "element_hessian.cuh"
 
 namespace jgs2 {
 
@@ -321,9 +322,24 @@ __device__ double tri_pair_derivs(const double* X, const double* bary, double* g
 }
 
 // Per pair: barrier energy, stencil gradient and PSD-projected Hessian
-// (contact.py:254-263 with project_spd=True).
-__global__ void k_pair_terms(int npairs, const double* rows, const double* x, const double* planes,
-                             double dhat, double kappa, double* pg, double* ph, double* pe) {
+// (contact.py:254-263 with project_spd=True). A vertex-triangle distance is
+// translation invariant, so its 12x12 barrier Hessian lives in the 9-dim
+// complement of the 3 translations: with the orthonormal basis
+// U = [h_m (x) e_c], h = (1,1,-1,-1)/2, (1,-1,1,-1)/2, (1,-1,-1,1)/2 over the
+// stencil (x, a, b, c), M = U^T H U (9x9) is projected (same tred2/tql2 as the
+// element Hessians) and H+ = U M+ U^T; the translation eigenvalues are 0 and
+// stay 0 under the reference's 12x12 eigh clamp.
+constexpr int kPairThreads = 64;
+__device__ __forceinline__ double hsign(int m, int p) {  // h_m[p] * 2
+  // m = 0: (1,1,-1,-1), 1: (1,-1,1,-1), 2: (1,-1,-1,1)
+  int b = m == 0 ? (p >> 1) : (m == 1 ? (p & 1) : ((p >> 1) ^ (p & 1)));
+  return b ? -1.0 : 1.0;
+}
+
+__global__ void __launch_bounds__(kPairThreads)
+k_pair_terms(int npairs, const double* rows, const double* x, const double* planes, double dhat, double kappa,
+             double* pg, double* ph, double* pe) {
+  extern __shared__ double psm[];
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= npairs) return;
   const double* r = rows + (size_t)kPairRow * k;
@@ -363,26 +379,56 @@ __global__ void k_pair_terms(int npairs, const double* rows, const double* x, co
   double gd[12], Hd[144];
   double d = tri_pair_derivs(X, r + 7, gd, Hd);
   Barrier B = barrier_fn(d, dhat, kappa);
-  double a[144];
-  for (int i = 0; i < 12; ++i) {
-    g[i] = B.db * gd[i];
-    for (int j = 0; j < 12; ++j) a[12 * i + j] = B.ddb * gd[i] * gd[j] + B.db * Hd[12 * i + j];
-  }
-  for (int i = 0; i < 12; ++i)
-    for (int j = i + 1; j < 12; ++j) {
-      double s = 0.5 * (a[12 * i + j] + a[12 * j + i]);
-      a[12 * i + j] = a[12 * j + i] = s;
-    }
-  double V[144];
-  jacobi_eig<12>(a, V, 30);
-  double lam[12];
-  for (int i = 0; i < 12; ++i) lam[i] = fmax(a[13 * i], 0.0);
-  for (int i = 0; i < 12; ++i)
-    for (int j = 0; j < 12; ++j) {
+  for (int i = 0; i < 12; ++i) g[i] = B.db * gd[i];
+  // complement coordinates: index q = 3 m + c
+  double G[9];
+  for (int m = 0; m < 3; ++m)
+    for (int c = 0; c < 3; ++c) {
       double s = 0.0;
-      for (int q = 0; q < 12; ++q) s += V[12 * i + q] * lam[q] * V[12 * j + q];
-      H[12 * i + j] = s;
+      for (int p = 0; p < 4; ++p) s += hsign(m, p) * gd[3 * p + c];
+      G[3 * m + c] = 0.5 * s;
     }
+  double* Vs = psm + threadIdx.x;
+  for (int qi = 0; qi < 9; ++qi) {
+    int mi = qi / 3, ci = qi % 3;
+    for (int qj = 0; qj <= qi; ++qj) {
+      int mj = qj / 3, cj = qj % 3;
+      double s = 0.0;
+      for (int p = 0; p < 4; ++p) {
+        double hp = hsign(mi, p);
+        for (int q = 0; q < 4; ++q)
+          s += hp * hsign(mj, q) * 0.5 * (Hd[12 * (3 * p + ci) + 3 * q + cj] + Hd[12 * (3 * q + cj) + 3 * p + ci]);
+      }
+      double mij = B.ddb * G[qi] * G[qj] + B.db * (0.25 * s);
+      Vs[(9 * qi + qj) * kPairThreads] = mij;
+      Vs[(9 * qj + qi) * kPairThreads] = mij;
+    }
+  }
+  double dg[9], od[9];
+  sym_eig9_reg<kPairThreads>(Vs, dg, od);
+  double lam[9];
+  for (int q = 0; q < 9; ++q) lam[q] = fmax(dg[q], 0.0);
+  // M+ = V lam V^T, then H+ = U M+ U^T
+  double Mp[45];
+  for (int i = 0; i < 9; ++i)
+    for (int j = 0; j <= i; ++j) {
+      double acc = 0.0;
+      for (int q = 0; q < 9; ++q) acc += Vs[(9 * i + q) * kPairThreads] * lam[q] * Vs[(9 * j + q) * kPairThreads];
+      Mp[JGS2_PK(i, j)] = acc;
+    }
+  for (int p = 0; p < 4; ++p)
+    for (int ci = 0; ci < 3; ++ci)
+      for (int q = 0; q < 4; ++q)
+        for (int cj = 0; cj < 3; ++cj) {
+          double s = 0.0;
+          for (int mi = 0; mi < 3; ++mi)
+            for (int mj = 0; mj < 3; ++mj) {
+              int a = 3 * mi + ci, b = 3 * mj + cj;
+              double mab = a >= b ? Mp[JGS2_PK(a, b)] : Mp[JGS2_PK(b, a)];
+              s += hsign(mi, p) * hsign(mj, q) * mab;
+            }
+          H[12 * (3 * p + ci) + 3 * q + cj] = 0.25 * s;
+        }
   pe[k] = B.b;
 }
 
@@ -622,8 +668,8 @@ void contact_energy_at(Ctx& C, const double* dx, double gamma, int slot) {
 // gradients into g_asm.
 void contact_add_gradients(Ctx& C) {
   if (C.npairs == 0) return;
-  k_pair_terms<<<grid_for(C.npairs, 64), 64, 0, C.stream>>>(C.npairs, C.pairs, C.x, C.planes, C.dhat,
-                                                            C.kappa, C.pair_g, C.pair_h, C.pair_e);
+  k_pair_terms<<<grid_for(C.npairs, kPairThreads), kPairThreads, 81 * kPairThreads * sizeof(double), C.stream>>>(
+      C.npairs, C.pairs, C.x, C.planes, C.dhat, C.kappa, C.pair_g, C.pair_h, C.pair_e);
   C.check_launch();
   JGS2_CUDA(cudaMemsetAsync(C.vp_cnt, 0, (C.nv + 1) * sizeof(int), C.stream));
   k_vp_count<<<grid_for(C.npairs), kBlock, 0, C.stream>>>(C.npairs, C.pairs, C.vp_cnt);

@@ -410,7 +410,10 @@ __device__ __forceinline__ void sym_eig9_reg(double* V, double (&d)[9], double (
 // memory. The number of indefinite elements is accumulated with one
 // warp-aggregated atomic per warp (diagnostic only; results do not depend
 // on it).
-__global__ void __launch_bounds__(kHessThreads)
+#ifndef JGS2_HESS_MINBLOCKS
+#define JGS2_HESS_MINBLOCKS 2
+#endif
+__global__ void __launch_bounds__(kHessThreads, JGS2_HESS_MINBLOCKS)
 k_element_mplus(int n, const int* elems, const double* __restrict__ xs, const int4* __restrict__ tets,
                 const double* __restrict__ dminv, const double4* __restrict__ eprops, double* mplus,
                 int* count) {
