@@ -217,9 +217,8 @@ struct Ctx {
   int* flag_d = nullptr;       // infeasibility flag
   double grid_cell = 1.0;      // broadphase cell size
   TriGrid pair_grid;
-  HierList hier_tri, hier_vtx;
-  int* hier_vlev = nullptr;
-  int* hier_tlev = nullptr;
+  HierList hier;               // both hierarchical grids (hier_grid.cuh)
+  int* hier_lev = nullptr;     // per object (surface vertices, then triangles)
   unsigned* hier_masks = nullptr;
   double* bbox_part = nullptr;  // surface bounding-box reduction (hier_grid.cuh)
   double* bbox_res = nullptr;

@@ -124,74 +124,68 @@ __device__ __forceinline__ long long box_cells(const HierArgs& a, int L, const d
   return n;
 }
 
-// per-object levels (+ kHierBig) and level occupancy masks
-__global__ void k_hier_levels(HierArgs a, int* vlev, int* tlev, unsigned* vmask, unsigned* tmask) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
+// Objects are indexed o in [0, nsv + nst): surface vertices (sv index) first,
+// then surface triangles. Both grids share one sorted entry list: a vertex
+// entry's key is ncells + cell (vertex grid), a triangle entry's key is the
+// cell (triangle grid).
+
+// per-object levels (+ kHierBig) and level occupancy masks [vertices, triangles]
+__global__ void k_hier_levels(HierArgs a, int* lev, unsigned* masks) {
+  int o = blockIdx.x * blockDim.x + threadIdx.x;
+  int nsv = a.cd.nsv;
+  if (o >= nsv + a.cd.nst) return;
   double lo[3], hi[3];
   int c0[3], c1[3];
-  if (i < a.cd.nsv) {
-    int v = a.cd.sv[i];
-    double r = vtx_rho(a, v);
-    int l = hier_level(r, a.cell);
+  double r;
+  if (o < nsv) {
+    int v = a.cd.sv[o];
+    r = vtx_rho(a, v);
     vtx_box(a, v, r, lo, hi);
-    bool big = box_cells(a, l, lo, hi, c0, c1) > kHierMaxCells;
-    vlev[i] = l | (big ? kHierBig : 0);
-    atomicOr(vmask, 1u << l);
+  } else {
+    r = tri_rho(a, o - nsv);
+    tri_box(a, o - nsv, r, lo, hi);
   }
-  if (i < a.cd.nst) {
-    double r = tri_rho(a, i);
-    int l = hier_level(r, a.cell);
-    tri_box(a, i, r, lo, hi);
-    bool big = box_cells(a, l, lo, hi, c0, c1) > kHierMaxCells;
-    tlev[i] = l | (big ? kHierBig : 0);
-    atomicOr(tmask, 1u << l);
-  }
+  int l = hier_level(r, a.cell);
+  bool big = box_cells(a, l, lo, hi, c0, c1) > kHierMaxCells;
+  lev[o] = l | (big ? kHierBig : 0);
+  atomicOr(masks + (o < nsv ? 0 : 1), 1u << l);
 }
 
 // grid entries of one object: the cells of its box in every grid L >= its
 // level that the opposing side occupies (big objects: none)
 template <bool WRITE>
-__device__ __forceinline__ long long hier_entries(const HierArgs& a, const double* lo, const double* hi, int lev,
-                                                  unsigned mask, int id, unsigned* keys, int* ids, long long o) {
-  if (lev & kHierBig) return 0;
+__global__ void k_hier_entries(HierArgs a, const int* lev, const unsigned* masks, const long long* off,
+                               long long* cnt, unsigned* keys, int* ids) {
+  int o = blockIdx.x * blockDim.x + threadIdx.x;
+  int nsv = a.cd.nsv;
+  if (o >= nsv + a.cd.nst) return;
+  bool vert = o < nsv;
+  double lo[3], hi[3];
+  if (vert) vtx_box(a, a.cd.sv[o], vtx_rho(a, a.cd.sv[o]), lo, hi);
+  else tri_box(a, o - nsv, tri_rho(a, o - nsv), lo, hi);
+  int lv = lev[o];
   long long n = 0;
-  for (int L = lev; L < kHierLevels; ++L) {
-    if (!((mask >> L) & 1u)) continue;
-    int c0[3], c1[3];
-    long long nc = box_cells(a, L, lo, hi, c0, c1);
-    if (WRITE)
-      for (int k = c0[2]; k <= c1[2]; ++k)
-        for (int j = c0[1]; j <= c1[1]; ++j)
-          for (int i = c0[0]; i <= c1[0]; ++i) {
-            keys[o] = hier_cell(a, L, i, j, k);
-            ids[o] = id;
-            ++o;
-          }
-    n += nc;
+  if (!(lv & kHierBig)) {
+    unsigned mask = masks[vert ? 1 : 0];  // levels the opposing side occupies
+    unsigned base = vert ? a.g.ncells : 0u;
+    int id = vert ? o : o - nsv;
+    long long q = WRITE ? off[o] : 0;
+    for (int L = lv; L < kHierLevels; ++L) {
+      if (!((mask >> L) & 1u)) continue;
+      int c0[3], c1[3];
+      long long nc = box_cells(a, L, lo, hi, c0, c1);
+      if (WRITE)
+        for (int k = c0[2]; k <= c1[2]; ++k)
+          for (int j = c0[1]; j <= c1[1]; ++j)
+            for (int i = c0[0]; i <= c1[0]; ++i) {
+              keys[q] = base + hier_cell(a, L, i, j, k);
+              ids[q] = id;
+              ++q;
+            }
+      n += nc;
+    }
   }
-  return n;
-}
-
-template <bool WRITE>
-__global__ void k_hier_tri_entries(HierArgs a, const int* tlev, const unsigned* vmask, const long long* off,
-                                   long long* cnt, unsigned* keys, int* ids) {
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= a.cd.nst) return;
-  double lo[3], hi[3];
-  tri_box(a, t, tri_rho(a, t), lo, hi);
-  long long n = hier_entries<WRITE>(a, lo, hi, tlev[t], *vmask, t, keys, ids, WRITE ? off[t] : 0);
-  if (!WRITE) cnt[t] = n;
-}
-
-template <bool WRITE>
-__global__ void k_hier_vtx_entries(HierArgs a, const int* vlev, const unsigned* tmask, const long long* off,
-                                   long long* cnt, unsigned* keys, int* ids) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.cd.nsv) return;
-  double lo[3], hi[3];
-  vtx_box(a, a.cd.sv[i], vtx_rho(a, a.cd.sv[i]), lo, hi);
-  long long n = hier_entries<WRITE>(a, lo, hi, vlev[i], *tmask, i, keys, ids, WRITE ? off[i] : 0);
-  if (!WRITE) cnt[i] = n;
+  if (!WRITE) cnt[o] = n;
 }
 
 // per-cell [start, end) of the sorted entries (cells without entries keep 0, 0)
@@ -243,96 +237,86 @@ struct HierOut {
   }
 };
 
-// vertex-side queries: triangle grid at the vertex's level (big: all triangles)
+// One query per object: a vertex scans the triangle grid at its level (big:
+// all triangles but the big ones, which are the triangle side's), a triangle
+// the vertex grid at its level (big: all vertices). MIN: grid-stride with a
+// deterministic min reduction; COUNT / WRITE: one thread per object.
 template <int MODE>
-__global__ void k_hier_query_v(HierArgs a, const int* vlev, const int* tlev, const int* cstart, const int* cend,
-                               const int* tids, const long long* off, long long* cnt, int* cv, int* ct,
-                               double* partials, unsigned* counter, double* out) {
+__global__ void k_hier_query(HierArgs a, const int* lev, const int* cstart, const int* cend, const int* ids,
+                             const long long* off, long long* cnt, int* cv, int* ct, double* partials,
+                             unsigned* counter, double* out) {
   HierOut R;
   R.cv = cv; R.ct = ct;
-  int i0 = blockIdx.x * blockDim.x + threadIdx.x;
-  int stride = MODE == HIER_MIN ? gridDim.x * blockDim.x : a.cd.nsv;
-  for (int i = i0; i < a.cd.nsv; i += stride) {
-    int v = a.cd.sv[i];
-    int bv = a.cd.vbody[v];
-    if (MODE == HIER_WRITE) R.o = off[i];
-    int lev = vlev[i];
-    if (lev & kHierBig) {  // pairs with big triangles are the triangle side's
-      for (int t = 0; t < a.cd.nst; ++t)
-        if (a.cd.tbody[t] != bv && !(tlev[t] & kHierBig)) R.take<MODE>(a, v, t);
-    } else {
-      double lo[3], hi[3], tl[3], th[3];
-      vtx_box(a, v, vtx_rho(a, v), lo, hi);
-      double inv = level_inv(a, lev);
-      int c0[3], c1[3];
-      box_cells(a, lev, lo, hi, c0, c1);
-      for (int s = c0[2]; s <= c1[2]; ++s)
-        for (int q = c0[1]; q <= c1[1]; ++q)
-          for (int p = c0[0]; p <= c1[0]; ++p) {
-            unsigned cell = hier_cell(a, lev, p, q, s);
-            long long f = cstart[cell], l = cend[cell];
-            ++R.ncell;
-            visit_cross(f, l, bv, [&](long long e) { return a.cd.tbody[tids[e]]; }, [&](long long e) {
-              ++R.nent;
-              int t = tids[e];
-              if (MODE != HIER_MIN) {
-                tri_box(a, t, tri_rho(a, t), tl, th);
-                if (!owns_pair(a, lev, lo, tl, inv, p, q, s)) return;
-              }
-              R.take<MODE>(a, v, t);
-            });
-          }
-    }
-    if (MODE == HIER_COUNT) cnt[i] = R.n, R.n = 0;
-  }
-  R.flush(a);
-  if (MODE == HIER_MIN) grid_reduce<OP_MIN>(R.mn, partials, counter, out);
-}
-
-// triangle-side queries: vertex grid at the triangle's level (big: all vertices)
-template <int MODE>
-__global__ void k_hier_query_t(HierArgs a, const int* vlev, const int* tlev, const int* cstart, const int* cend,
-                               const int* vids, const long long* off, long long* cnt, int* cv, int* ct,
-                               double* partials, unsigned* counter, double* out) {
-  HierOut R;
-  R.cv = cv; R.ct = ct;
-  int t0 = blockIdx.x * blockDim.x + threadIdx.x;
-  int stride = MODE == HIER_MIN ? gridDim.x * blockDim.x : a.cd.nst;
-  for (int t = t0; t < a.cd.nst; t += stride) {
-    int bt = a.cd.tbody[t];
-    if (MODE == HIER_WRITE) R.o = off[t];
-    int lev = tlev[t];
-    if (lev & kHierBig) {
-      for (int i = 0; i < a.cd.nsv; ++i) {
-        int v = a.cd.sv[i];
-        if (a.cd.vbody[v] != bt) R.take<MODE>(a, v, t);
+  const int nsv = a.cd.nsv, nobj = nsv + a.cd.nst;
+  int o0 = blockIdx.x * blockDim.x + threadIdx.x;
+  int stride = MODE == HIER_MIN ? gridDim.x * blockDim.x : nobj;
+  for (int o = o0; o < nobj; o += stride) {
+    if (MODE == HIER_WRITE) R.o = off[o];
+    int lv = lev[o];
+    if (o < nsv) {  // ---- vertex side
+      int v = a.cd.sv[o];
+      int bv = a.cd.vbody[v];
+      if (lv & kHierBig) {
+        for (int t = 0; t < a.cd.nst; ++t)
+          if (a.cd.tbody[t] != bv && !(lev[nsv + t] & kHierBig)) R.take<MODE>(a, v, t);
+      } else {
+        double lo[3], hi[3], tl[3], th[3];
+        vtx_box(a, v, vtx_rho(a, v), lo, hi);
+        double inv = level_inv(a, lv);
+        int c0[3], c1[3];
+        box_cells(a, lv, lo, hi, c0, c1);
+        for (int s = c0[2]; s <= c1[2]; ++s)
+          for (int q = c0[1]; q <= c1[1]; ++q)
+            for (int p = c0[0]; p <= c1[0]; ++p) {
+              unsigned cell = hier_cell(a, lv, p, q, s);
+              long long f = cstart[cell], l = cend[cell];
+              ++R.ncell;
+              visit_cross(f, l, bv, [&](long long e) { return a.cd.tbody[ids[e]]; }, [&](long long e) {
+                ++R.nent;
+                int t = ids[e];
+                if (MODE != HIER_MIN) {
+                  tri_box(a, t, tri_rho(a, t), tl, th);
+                  if (!owns_pair(a, lv, lo, tl, inv, p, q, s)) return;
+                }
+                R.take<MODE>(a, v, t);
+              });
+            }
       }
-    } else {
-      double lo[3], hi[3], vl[3], vh[3];
-      tri_box(a, t, tri_rho(a, t), lo, hi);
-      double inv = level_inv(a, lev);
-      int c0[3], c1[3];
-      box_cells(a, lev, lo, hi, c0, c1);
-      for (int s = c0[2]; s <= c1[2]; ++s)
-        for (int q = c0[1]; q <= c1[1]; ++q)
-          for (int p = c0[0]; p <= c1[0]; ++p) {
-            unsigned cell = hier_cell(a, lev, p, q, s);
-            long long f = cstart[cell], l = cend[cell];
-            ++R.ncell;
-            visit_cross(f, l, bt, [&](long long e) { return a.cd.vbody[a.cd.sv[vids[e]]]; }, [&](long long e) {
-              ++R.nent;
-              int i = vids[e];
-              int v = a.cd.sv[i];
-              if (MODE != HIER_MIN) {
-                if ((vlev[i] & ~kHierBig) >= lev) return;  // level tie: the vertex side has it
-                vtx_box(a, v, vtx_rho(a, v), vl, vh);
-                if (!owns_pair(a, lev, lo, vl, inv, p, q, s)) return;
-              }
-              R.take<MODE>(a, v, t);
-            });
-          }
+    } else {  // ---- triangle side
+      int t = o - nsv;
+      int bt = a.cd.tbody[t];
+      if (lv & kHierBig) {
+        for (int i = 0; i < nsv; ++i) {
+          int v = a.cd.sv[i];
+          if (a.cd.vbody[v] != bt) R.take<MODE>(a, v, t);
+        }
+      } else {
+        double lo[3], hi[3], vl[3], vh[3];
+        tri_box(a, t, tri_rho(a, t), lo, hi);
+        double inv = level_inv(a, lv);
+        int c0[3], c1[3];
+        box_cells(a, lv, lo, hi, c0, c1);
+        for (int s = c0[2]; s <= c1[2]; ++s)
+          for (int q = c0[1]; q <= c1[1]; ++q)
+            for (int p = c0[0]; p <= c1[0]; ++p) {
+              unsigned cell = a.g.ncells + hier_cell(a, lv, p, q, s);
+              long long f = cstart[cell], l = cend[cell];
+              ++R.ncell;
+              visit_cross(f, l, bt, [&](long long e) { return a.cd.vbody[a.cd.sv[ids[e]]]; }, [&](long long e) {
+                ++R.nent;
+                int i = ids[e];
+                int v = a.cd.sv[i];
+                if (MODE != HIER_MIN) {
+                  if ((lev[i] & ~kHierBig) >= lv) return;  // level tie: the vertex side has it
+                  vtx_box(a, v, vtx_rho(a, v), vl, vh);
+                  if (!owns_pair(a, lv, lo, vl, inv, p, q, s)) return;
+                }
+                R.take<MODE>(a, v, t);
+              });
+            }
+      }
     }
-    if (MODE == HIER_COUNT) cnt[t] = R.n, R.n = 0;
+    if (MODE == HIER_COUNT) cnt[o] = R.n, R.n = 0;
   }
   R.flush(a);
   if (MODE == HIER_MIN) grid_reduce<OP_MIN>(R.mn, partials, counter, out);
@@ -398,12 +382,6 @@ inline void hier_geometry(Ctx& C, const double* x, HierArgs& a) {
   a.g.ncells = off;
 }
 
-inline void hier_alloc(Ctx& C, HierList& h, int nobj) {
-  if (h.cnt) return;
-  h.cnt = C.alloc<long long>(nobj + 1);
-  h.off = C.alloc<long long>(nobj + 1);
-}
-
 // exclusive scan of n+1 counts (last one zeroed) -> off; returns the total
 inline long long scan_counts(Ctx& C, long long* cnt, long long* off, long long n) {
   JGS2_CUDA(cudaMemsetAsync(cnt + n, 0, sizeof(long long), C.stream));
@@ -418,17 +396,31 @@ inline long long scan_counts(Ctx& C, long long* cnt, long long* off, long long n
   return total;
 }
 
-template <class CountK, class WriteK>
-inline void hier_build(Ctx& C, HierList& h, int nobj, unsigned ncells, CountK count, WriteK write) {
-  hier_alloc(C, h, nobj);
-  if ((long long)ncells > h.ncells_cap) {
-    h.cstart = C.alloc<int>(ncells);
-    h.cend = C.alloc<int>(ncells);
-    h.ncells_cap = ncells;
+// geometry, levels, both grids (one sorted list) and the cell directory for
+// radii b * s + pad. Two host syncs (bounding box, entry count).
+inline void hier_prepare(Ctx& C, HierArgs& a, const double* x) {
+  hier_geometry(C, x, a);
+  HierList& h = C.hier;
+  int nobj = C.nsv + C.nst;
+  if (!C.hier_lev) {
+    C.hier_lev = C.alloc<int>(nobj + 1);
+    C.hier_masks = C.alloc<unsigned>(2);
+    h.cnt = C.alloc<long long>(nobj + 1);
+    h.off = C.alloc<long long>(nobj + 1);
   }
-  JGS2_CUDA(cudaMemsetAsync(h.cstart, 0, ncells * sizeof(int), C.stream));
-  JGS2_CUDA(cudaMemsetAsync(h.cend, 0, ncells * sizeof(int), C.stream));
-  count(h);
+  unsigned ndir = 2 * a.g.ncells;
+  if ((long long)ndir > h.ncells_cap) {
+    h.cstart = C.alloc<int>(ndir);
+    h.cend = C.alloc<int>(ndir);
+    h.ncells_cap = ndir;
+  }
+  JGS2_CUDA(cudaMemsetAsync(C.hier_masks, 0, 2 * sizeof(unsigned), C.stream));
+  JGS2_CUDA(cudaMemsetAsync(h.cstart, 0, ndir * sizeof(int), C.stream));
+  JGS2_CUDA(cudaMemsetAsync(h.cend, 0, ndir * sizeof(int), C.stream));
+  k_hier_levels<<<grid_for(nobj), kBlock, 0, C.stream>>>(a, C.hier_lev, C.hier_masks);
+  C.check_launch();
+  k_hier_entries<false><<<grid_for(nobj), kBlock, 0, C.stream>>>(a, C.hier_lev, C.hier_masks, nullptr, h.cnt,
+                                                                nullptr, nullptr);
   C.check_launch();
   long long total = scan_counts(C, h.cnt, h.off, nobj);
   if (total < 0 || total > (long long)INT32_MAX)
@@ -441,10 +433,11 @@ inline void hier_build(Ctx& C, HierList& h, int nobj, unsigned ncells, CountK co
   }
   h.n = total;
   if (total == 0) return;
-  write(h);
+  k_hier_entries<true><<<grid_for(nobj), kBlock, 0, C.stream>>>(a, C.hier_lev, C.hier_masks, h.off, nullptr,
+                                                               h.ka, h.ia);
   C.check_launch();
   int bits = 1;
-  while (bits < 32 && (1ull << bits) < (unsigned long long)ncells) ++bits;
+  while (bits < 32 && (1ull << bits) < (unsigned long long)ndir) ++bits;
   size_t sb = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, sb, h.ka, h.kb, h.ia, h.ib, (int)total, 0, bits, C.stream);
   if (sb > C.scan_temp_bytes) { C.scan_temp = C.alloc<char>(sb); C.scan_temp_bytes = sb; }
@@ -453,39 +446,6 @@ inline void hier_build(Ctx& C, HierList& h, int nobj, unsigned ncells, CountK co
   ++C.launches;
   k_hier_dir<<<grid_for(total), kBlock, 0, C.stream>>>(h.kb, total, h.cstart, h.cend);
   C.check_launch();
-}
-
-// levels + both grids for radii b * s + pad
-inline void hier_prepare(Ctx& C, HierArgs& a, const double* x) {
-  hier_geometry(C, x, a);
-  if (!C.hier_vlev) {
-    C.hier_vlev = C.alloc<int>(C.nsv + 1);
-    C.hier_tlev = C.alloc<int>(C.nst + 1);
-    C.hier_masks = C.alloc<unsigned>(2);
-  }
-  JGS2_CUDA(cudaMemsetAsync(C.hier_masks, 0, 2 * sizeof(unsigned), C.stream));
-  int nmax = std::max(C.nsv, C.nst);
-  k_hier_levels<<<grid_for(nmax), kBlock, 0, C.stream>>>(a, C.hier_vlev, C.hier_tlev, C.hier_masks,
-                                                         C.hier_masks + 1);
-  C.check_launch();
-  hier_build(C, C.hier_tri, C.nst, a.g.ncells,
-             [&](HierList& h) {
-               k_hier_tri_entries<false><<<grid_for(C.nst), kBlock, 0, C.stream>>>(
-                   a, C.hier_tlev, C.hier_masks, nullptr, h.cnt, nullptr, nullptr);
-             },
-             [&](HierList& h) {
-               k_hier_tri_entries<true><<<grid_for(C.nst), kBlock, 0, C.stream>>>(
-                   a, C.hier_tlev, C.hier_masks, h.off, nullptr, h.ka, h.ia);
-             });
-  hier_build(C, C.hier_vtx, C.nsv, a.g.ncells,
-             [&](HierList& h) {
-               k_hier_vtx_entries<false><<<grid_for(C.nsv), kBlock, 0, C.stream>>>(
-                   a, C.hier_vlev, C.hier_masks + 1, nullptr, h.cnt, nullptr, nullptr);
-             },
-             [&](HierList& h) {
-               k_hier_vtx_entries<true><<<grid_for(C.nsv), kBlock, 0, C.stream>>>(
-                   a, C.hier_vlev, C.hier_masks + 1, h.off, nullptr, h.ka, h.ia);
-             });
 }
 
 // min over cross-body pairs of dist / rate among the pairs with rate < b
@@ -497,7 +457,6 @@ inline double hier_min_ratio(Ctx& C, const double* x, const double* dx, double b
   a.dx = dx;
   a.b = b;
   a.pad = 0.0;
-  a.cell = C.grid_cell;
   a.dlim = 0.0;
   bool dbg = getenv("JGS2_DEBUG_HIER") != nullptr;
   auto now = [&]() { if (dbg) C.sync(); return std::chrono::steady_clock::now(); };
@@ -510,20 +469,14 @@ inline double hier_min_ratio(Ctx& C, const double* x, const double* dx, double b
   auto t0 = now();
   hier_prepare(C, a, x);
   auto t1 = now();
-  const HierList& T = C.hier_tri;
-  const HierList& V = C.hier_vtx;
-  double* part = C.partials + R_CAP * kMaxPartials;
-  double m[2] = {INFINITY, INFINITY};
-  k_hier_query_v<HIER_MIN><<<red_grid(C.nsv), kBlock, 0, C.stream>>>(
-      a, C.hier_vlev, C.hier_tlev, T.cstart, T.cend, T.ib, nullptr, nullptr, nullptr, nullptr, part,
+  const HierList& h = C.hier;
+  double m = INFINITY;
+  int nobj = C.nsv + C.nst;
+  k_hier_query<HIER_MIN><<<red_grid(nobj), kBlock, 0, C.stream>>>(
+      a, C.hier_lev, h.cstart, h.cend, h.ib, nullptr, nullptr, nullptr, nullptr, C.partials + R_CAP * kMaxPartials,
       C.counters + R_CAP, C.res + R_CAP);
   C.check_launch();
-  JGS2_CUDA(cudaMemcpyAsync(&m[0], C.res + R_CAP, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
-  k_hier_query_t<HIER_MIN><<<red_grid(C.nst), kBlock, 0, C.stream>>>(
-      a, C.hier_vlev, C.hier_tlev, V.cstart, V.cend, V.ib, nullptr, nullptr, nullptr, nullptr, part,
-      C.counters + R_CAP, C.res + R_CAP);
-  C.check_launch();
-  JGS2_CUDA(cudaMemcpyAsync(&m[1], C.res + R_CAP, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+  JGS2_CUDA(cudaMemcpyAsync(&m, C.res + R_CAP, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
   C.sync();
   if (dbg) {
     auto t2 = now();
@@ -533,11 +486,11 @@ inline double hier_min_ratio(Ctx& C, const double* x, const double* dx, double b
     unsigned long long hs[3];
     JGS2_CUDA(cudaMemcpy(hs, st, sizeof(hs), cudaMemcpyDeviceToHost));
     cudaFree(st);
-    fprintf(stderr, "hier_min_ratio b=%.3e cell=%.3e ncells=%u entries tri=%lld vtx=%lld masks v=%x t=%x m=%.3e %.3e "
+    fprintf(stderr, "hier_min_ratio b=%.3e cell=%.3e ncells=%u entries=%lld masks v=%x t=%x m=%.3e "
             "ms prep %.2f q %.2f | cells %llu cross %llu pairs %llu\n",
-            a.b, a.cell, a.g.ncells, T.n, V.n, mk[0], mk[1], m[0], m[1], ms(t0, t1), ms(t1, t2), hs[0], hs[1], hs[2]);
+            a.b, a.cell, a.g.ncells, h.n, mk[0], mk[1], m, ms(t0, t1), ms(t1, t2), hs[0], hs[1], hs[2]);
   }
-  return std::fmin(m[0], m[1]);
+  return m;
 }
 
 // min over cross-body pairs of dist / rate among pairs that can lower
@@ -575,25 +528,16 @@ inline long long hier_candidates(Ctx& C, const double* x, const double* dx, doub
   a.dx = dx;
   a.b = gmax * (1.0 + 1e-6);
   a.pad = 0.5 * C.dhat * (1.0 + 1e-6);
-  a.cell = C.grid_cell;
   a.dlim = 2.0 * a.pad;
   hier_prepare(C, a, x);
-  const HierList& T = C.hier_tri;
-  const HierList& V = C.hier_vtx;
-  long long nobj = (long long)C.nsv + C.nst;
+  const HierList& h = C.hier;
+  int nobj = C.nsv + C.nst;
   if (!C.cand_cnt) {
     C.cand_cnt = C.alloc<long long>(nobj + 1);
     C.cand_off = C.alloc<long long>(nobj + 1);
   }
-  long long* cv_cnt = C.cand_cnt;
-  long long* ct_cnt = C.cand_cnt + C.nsv;
-  k_hier_query_v<HIER_COUNT><<<grid_for(C.nsv), kBlock, 0, C.stream>>>(
-      a, C.hier_vlev, C.hier_tlev, T.cstart, T.cend, T.ib, nullptr, cv_cnt, nullptr, nullptr, nullptr, nullptr,
-      nullptr);
-  C.check_launch();
-  k_hier_query_t<HIER_COUNT><<<grid_for(C.nst), kBlock, 0, C.stream>>>(
-      a, C.hier_vlev, C.hier_tlev, V.cstart, V.cend, V.ib, nullptr, ct_cnt, nullptr, nullptr, nullptr, nullptr,
-      nullptr);
+  k_hier_query<HIER_COUNT><<<grid_for(nobj), kBlock, 0, C.stream>>>(
+      a, C.hier_lev, h.cstart, h.cend, h.ib, nullptr, C.cand_cnt, nullptr, nullptr, nullptr, nullptr, nullptr);
   C.check_launch();
   long long total = scan_counts(C, C.cand_cnt, C.cand_off, nobj);
   if (total > budget) return -1;
@@ -604,13 +548,8 @@ inline long long hier_candidates(Ctx& C, const double* x, const double* dx, doub
     C.cand_cap = cap;
   }
   if (total == 0) return 0;
-  k_hier_query_v<HIER_WRITE><<<grid_for(C.nsv), kBlock, 0, C.stream>>>(
-      a, C.hier_vlev, C.hier_tlev, T.cstart, T.cend, T.ib, C.cand_off, nullptr, C.cand_v, C.cand_t, nullptr,
-      nullptr, nullptr);
-  C.check_launch();
-  k_hier_query_t<HIER_WRITE><<<grid_for(C.nst), kBlock, 0, C.stream>>>(
-      a, C.hier_vlev, C.hier_tlev, V.cstart, V.cend, V.ib, C.cand_off + C.nsv, nullptr, C.cand_v, C.cand_t,
-      nullptr, nullptr, nullptr);
+  k_hier_query<HIER_WRITE><<<grid_for(nobj), kBlock, 0, C.stream>>>(
+      a, C.hier_lev, h.cstart, h.cend, h.ib, C.cand_off, nullptr, C.cand_v, C.cand_t, nullptr, nullptr, nullptr);
   C.check_launch();
   return total;
 }
