@@ -133,22 +133,31 @@ __device__ __forceinline__ long long box_cells(const HierArgs& a, int L, const d
 __global__ void k_hier_levels(HierArgs a, int* lev, unsigned* masks) {
   int o = blockIdx.x * blockDim.x + threadIdx.x;
   int nsv = a.cd.nsv;
-  if (o >= nsv + a.cd.nst) return;
-  double lo[3], hi[3];
-  int c0[3], c1[3];
-  double r;
-  if (o < nsv) {
-    int v = a.cd.sv[o];
-    r = vtx_rho(a, v);
-    vtx_box(a, v, r, lo, hi);
-  } else {
-    r = tri_rho(a, o - nsv);
-    tri_box(a, o - nsv, r, lo, hi);
+  unsigned vbit = 0, tbit = 0;
+  if (o < nsv + a.cd.nst) {
+    double lo[3], hi[3];
+    int c0[3], c1[3];
+    double r;
+    if (o < nsv) {
+      int v = a.cd.sv[o];
+      r = vtx_rho(a, v);
+      vtx_box(a, v, r, lo, hi);
+    } else {
+      r = tri_rho(a, o - nsv);
+      tri_box(a, o - nsv, r, lo, hi);
+    }
+    int l = hier_level(r, a.cell);
+    bool big = box_cells(a, l, lo, hi, c0, c1) > kHierMaxCells;
+    lev[o] = l | (big ? kHierBig : 0);
+    (o < nsv ? vbit : tbit) = 1u << l;
   }
-  int l = hier_level(r, a.cell);
-  bool big = box_cells(a, l, lo, hi, c0, c1) > kHierMaxCells;
-  lev[o] = l | (big ? kHierBig : 0);
-  atomicOr(masks + (o < nsv ? 0 : 1), 1u << l);
+  // one atomic per warp and side (a same-address atomic per thread serialises)
+  vbit = __reduce_or_sync(0xffffffffu, vbit);
+  tbit = __reduce_or_sync(0xffffffffu, tbit);
+  if ((threadIdx.x & 31) == 0) {
+    if (vbit) atomicOr(masks, vbit);
+    if (tbit) atomicOr(masks + 1, tbit);
+  }
 }
 
 // grid entries of one object: the cells of its box in every grid L >= its
