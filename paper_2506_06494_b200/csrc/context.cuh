@@ -91,6 +91,8 @@ struct Factor {
   std::vector<int> level_ptr;  // host
   std::vector<int> level_maxnf;
   int4* fwd_tasks = nullptr;   // (front, row_begin, row_end)
+  int4* fwdn_tasks = nullptr;  // narrow fronts: (front, 64-row chunk)
+  std::vector<int> fwdn_level_ptr;
   int4* bwd_tasks = nullptr;   // (front, col_begin, col_end)
   std::vector<int> fwd_level_ptr, bwd_level_ptr, fwd_level_smem, bwd_level_smem;
   std::vector<int64_t> asm_level_ptr, gat_level_ptr;

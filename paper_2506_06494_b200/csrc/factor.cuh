@@ -198,6 +198,59 @@ k_fwd_apply(const int4* tasks, int ntasks, const int* colbeg, const int* f_ns, c
   }
 }
 
+// forward apply for narrow fronts (ns <= kNarrowCols: the leaves and the
+// small separators of the lower levels), task = (front, 64-row chunk): one
+// warp per task, lanes own row pairs across all columns, v broadcast from
+// L1. No shared memory and no block barriers (the block-level kernel's
+// per-64-row cross-warp reduction dominates on narrow panels).
+constexpr int kNarrowCols = 128;
+__global__ void __launch_bounds__(kSolveThreads)
+k_fwd_apply_narrow(const int4* tasks, int ntasks, const int* colbeg, const int* f_ns, const int* f_nr,
+                   const int* f_ld, const int64_t* loff, const int64_t* uoff, const int64_t* woff,
+                   const double* __restrict__ L, const double* __restrict__ w, double* b, double* u) {
+  int lane = threadIdx.x & 31;
+  int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = w0; t < ntasks; t += nw) {
+    int4 tk = tasks[t];
+    int f = tk.x, r0 = tk.y, r1 = tk.z;
+    int ns = f_ns[f], ld = f_ld[f];
+    const double* P = L + loff[f];
+    const double* v = w + woff[f];
+    int row = r0 + 2 * lane;
+    if (row >= r1) continue;
+    int cend = min(ns, r1);
+    const double2* Pr = reinterpret_cast<const double2*>(P + row);
+    const int64_t s2 = (int64_t)ld / 2;
+    double a0 = 0, a1 = 0, a2 = 0, a3 = 0, c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+    int j = 0;
+    for (; j + 3 < cend; j += 4) {
+      double2 p0 = __ldg(Pr + (int64_t)j * s2);
+      double2 p1 = __ldg(Pr + (int64_t)(j + 1) * s2);
+      double2 p2 = __ldg(Pr + (int64_t)(j + 2) * s2);
+      double2 p3 = __ldg(Pr + (int64_t)(j + 3) * s2);
+      double v0 = __ldg(v + j), v1 = __ldg(v + j + 1), v2 = __ldg(v + j + 2), v3 = __ldg(v + j + 3);
+      a0 += p0.x * v0; c0 += p0.y * v0;
+      a1 += p1.x * v1; c1 += p1.y * v1;
+      a2 += p2.x * v2; c2 += p2.y * v2;
+      a3 += p3.x * v3; c3 += p3.y * v3;
+    }
+    for (; j < cend; ++j) {
+      double2 p0 = __ldg(Pr + (int64_t)j * s2);
+      double v0 = __ldg(v + j);
+      a0 += p0.x * v0; c0 += p0.y * v0;
+    }
+    double t0 = (a0 + a1) + (a2 + a3), t1 = (c0 + c1) + (c2 + c3);
+    int cb = colbeg[f];
+    int64_t uo = uoff[f];
+    if (row < ns) b[cb + row] = t0;
+    else u[uo + (row - ns)] = v[row] - t0;
+    if (row + 1 < r1) {
+      if (row + 1 < ns) b[cb + row + 1] = t1;
+      else u[uo + (row + 1 - ns)] = v[row + 1] - t1;
+    }
+  }
+}
+
 // flat forward assembly: w[dst] = b[bsrc] (or 0) + sum of the children's
 // update entries mapped to this position (child order, deterministic)
 __global__ void k_fwd_assemble_flat(int64_t n, const int64_t* dst, const int* bsrc, const int64_t* cp,
@@ -399,8 +452,9 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
   // multiples of 32 rows) / column blocks (backward, multiples of 8
   // columns) of roughly equal entry counts; enough tasks to fill 2 waves.
   {
-    std::vector<int4> ft, bt;
+    std::vector<int4> ft, bt, fn;
     F.fwd_level_ptr.assign(F.nlevels + 1, 0);
+    F.fwdn_level_ptr.assign(F.nlevels + 1, 0);
     F.bwd_level_ptr.assign(F.nlevels + 1, 0);
     F.fwd_level_smem.assign(F.nlevels, 0);
     F.bwd_level_smem.assign(F.nlevels, 0);
@@ -418,7 +472,11 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
         // forward rows
         int r0 = 0;
         double acc = 0;
-        for (int i0 = 0; i0 < nf; i0 += 64) {
+        if (ns <= kNarrowCols) {  // narrow front: one warp task per 64-row chunk
+          for (int i0 = 0; i0 < nf; i0 += 64) fn.push_back(make_int4(f, i0, std::min(nf, i0 + 64), 0));
+          r0 = nf;
+        }
+        for (int i0 = r0; i0 < nf; i0 += 64) {
           int rows = std::min(64, nf - i0);
           int cols = std::min(ns, i0 + 64);
           acc += (double)rows * std::max(cols, 1);
@@ -446,9 +504,11 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
         }
       }
       F.fwd_level_ptr[l + 1] = (int)ft.size();
+      F.fwdn_level_ptr[l + 1] = (int)fn.size();
       F.bwd_level_ptr[l + 1] = (int)bt.size();
     }
     F.fwd_tasks = C.upload(ft.data(), ft.size());
+    F.fwdn_tasks = C.upload(fn.data(), fn.size());
     // flat per-level assemble map (forward) and gather map (backward):
     // one entry per front position; contributions in child order.
     std::vector<int64_t> adst, acp(1, 0), asrc, gdst;
@@ -682,11 +742,19 @@ void factor_solve_launches(Ctx& C) {
     int64_t na = F.asm_level_ptr[l + 1] - F.asm_level_ptr[l];
     int64_t o = F.asm_level_ptr[l];
     int nt = F.fwd_level_ptr[l + 1] - F.fwd_level_ptr[l];
-    if (na == 0 && nt == 0) continue;  // level of zero-size joining fronts
+    int nn = F.fwdn_level_ptr[l + 1] - F.fwdn_level_ptr[l];
+    if (na == 0 && nt == 0 && nn == 0) continue;  // level of zero-size joining fronts
     if (na > 0)
     k_fwd_assemble_flat<<<grid_for(na), kBlock, 0, C.stream>>>(na, F.asm_dst + o, F.asm_b + o,
                                                                F.asm_cp + o, F.asm_src, C.b, F.u, F.w);
     C.check_launch();
+    if (nn > 0) {
+      int gn = std::min((nn + 7) / 8, 148 * 8);
+      k_fwd_apply_narrow<<<gn, kSolveThreads, 0, C.stream>>>(F.fwdn_tasks + F.fwdn_level_ptr[l], nn,
+                                                             F.f_colbeg, F.f_ns, F.f_nr, F.f_ld, F.f_loff,
+                                                             F.f_uoff, F.f_woff, F.L, F.w, C.b, F.u);
+      C.check_launch();
+    }
     if (nt == 0) continue;
     int g = std::min(nt, 148 * kApplyCtasPerSm);
     k_fwd_apply<<<g, kSolveThreads, 0, C.stream>>>(F.fwd_tasks + F.fwd_level_ptr[l], nt, F.f_colbeg,
