@@ -302,7 +302,7 @@ __device__ void sampled_inner(const DevModel& m, const LocalArgs& a, int v, doub
   }
 }
 
-__global__ void __launch_bounds__(kBlock)
+__global__ void __launch_bounds__(128, 4)
 k_local(DevModel m, LocalArgs a) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m.nfree) return;

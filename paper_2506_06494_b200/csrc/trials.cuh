@@ -36,7 +36,9 @@ __device__ void block_reduce_multi(double* acc, int n, double* partials) {
   }
 }
 
-__global__ void __launch_bounds__(kBlock)
+// 2 blocks per SM (<= 128 registers): at 155 registers one 256-thread block
+// per SM left the FP64 pipes latency-bound (ncu: 12.5% occupancy)
+__global__ void __launch_bounds__(kBlock, 2)
 k_energy_batch(DevModel m, const double* __restrict__ x0, const double* __restrict__ dx, Gammas G,
                const double* __restrict__ z, double h, double* partials) {
   double acc[kTrialBatch];
