@@ -684,39 +684,50 @@ void contact_add_gradients(Ctx& C) {
   C.check_launch();
 }
 
-inline double hier_cap_min(Ctx& C, const double* x, const double* dx, double cap_ub);
+inline double hier_cap_min(Ctx& C, const double* x, const double* dx, double cap_ub, double smax,
+                           const double* bb);
+inline void hier_bbox_launch(Ctx& C, const double* x, double* out);
 
 // feasibility_step_cap (assembly.py:263-291). pairs_at_x: the pair table
 // holds the pairs detected at this x (their d equal the reference's
 // closest-point distances bitwise) and gives an upper bound cap_ub; only
 // pairs with dist < cap_ub (s_v + s_t) / 0.9 can lower it further, so the
-// grid radii scale with cap_ub (exact).
-double contact_step_cap(Ctx& C, const double* x, const double* dx, bool pairs_at_x = false) {
+// grid radii scale with cap_ub (exact). The plane, pair-table, max-step and
+// bounding-box reductions share one host sync; bb_out (6 doubles, may be
+// null) receives the surface bounding box at x for later grids.
+double contact_step_cap(Ctx& C, const double* x, const double* dx, bool pairs_at_x = false,
+                        double* bb_out = nullptr) {
   ContactDev cd = contactdev(C);
-  double cap = 1.0;
-  auto read_min = [&](double* m) {
-    JGS2_CUDA(cudaMemcpyAsync(m, C.res + R_CAP, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
-    C.sync();
-  };
+  bool tri = use_tri_grid(C);
+  bool pt = tri && pairs_at_x && C.npairs > 0;
+  if (!C.bbox_res) C.bbox_res = C.alloc<double>(6);
   if (C.nplanes > 0) {
     k_cap_planes<<<red_grid(C.nsv * C.nplanes), kBlock, 0, C.stream>>>(
         cd, x, dx, C.partials + R_CAP * kMaxPartials, C.counters + R_CAP, C.res + R_CAP);
     C.check_launch();
-    double m = 0;
-    read_min(&m);
-    if (std::isfinite(m)) cap = std::min(cap, 0.9 * m);
   }
-  if (use_tri_grid(C)) {
-    if (pairs_at_x && C.npairs > 0) {
-      k_cap_pairtable<<<std::min(grid_for(C.npairs), 256), kBlock, 0, C.stream>>>(
-          C.npairs, C.pairs, dx, C.partials + R_CAP * kMaxPartials, C.counters + R_CAP, C.res + R_CAP);
-      C.check_launch();
-      double m = 0;
-      read_min(&m);
-      if (std::isfinite(m)) cap = std::min(cap, 0.9 * m);
-    }
+  if (pt) {
+    k_cap_pairtable<<<std::min(grid_for(C.npairs), 256), kBlock, 0, C.stream>>>(
+        C.npairs, C.pairs, dx, C.partials + R_CAP2 * kMaxPartials, C.counters + R_CAP2, C.res + R_CAP2);
+    C.check_launch();
+  }
+  if (tri) {
+    k_sv_maxstep<<<red_grid(C.nsv), kBlock, 0, C.stream>>>(cd, dx, C.partials + R_AUX * kMaxPartials,
+                                                           C.counters + R_AUX, C.res + R_AUX);
+    C.check_launch();
+    hier_bbox_launch(C, x, C.bbox_res);
+  }
+  double* h = C.h_res + 40;  // pinned scratch: res slots + bounding box
+  JGS2_CUDA(cudaMemcpyAsync(h, C.res, R_NSLOTS * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+  if (tri) JGS2_CUDA(cudaMemcpyAsync(h + R_NSLOTS, C.bbox_res, 6 * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+  C.sync();
+  double cap = 1.0;
+  if (C.nplanes > 0 && std::isfinite(h[R_CAP])) cap = std::min(cap, 0.9 * h[R_CAP]);
+  if (pt && std::isfinite(h[R_CAP2])) cap = std::min(cap, 0.9 * h[R_CAP2]);
+  if (tri) {
+    if (bb_out) memcpy(bb_out, h + R_NSLOTS, 6 * sizeof(double));
     if (!(cap > 0)) return std::max(cap, 0.0);
-    double m = hier_cap_min(C, x, dx, cap);
+    double m = hier_cap_min(C, x, dx, cap, h[R_AUX], h + R_NSLOTS);
     if (std::isfinite(m)) cap = std::min(cap, 0.9 * m);
   }
   return std::max(cap, 0.0);

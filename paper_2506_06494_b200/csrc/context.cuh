@@ -38,7 +38,8 @@ enum ResSlot {
   R_DXMAX,        // max_v |dx_v|
   R_CAP,          // feasibility cap (min)
   R_EBEFORE,      // energy at the sweep start
-  R_AUX,          // scratch (barrier sum)
+  R_AUX,          // scratch (barrier sum, max step)
+  R_CAP2,         // feasibility cap: active pair-table bound
   R_NSLOTS = 8
 };
 

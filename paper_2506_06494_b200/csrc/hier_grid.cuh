@@ -354,24 +354,33 @@ __global__ void k_bbox_final(const double* part, int nb, double* out) {
   }
 }
 
-// level-0 cell and the dense per-level grids over the surface's bounding box
-inline void hier_geometry(Ctx& C, const double* x, HierArgs& a) {
-  if (!C.bbox_part) {
-    C.bbox_part = C.alloc<double>(6 * kMaxPartials);
-    C.bbox_res = C.alloc<double>(6);
-  }
+// bounding box of the surface at x, reduced on the device into out[6]
+// (min xyz, -max xyz); no host sync
+inline void hier_bbox_launch(Ctx& C, const double* x, double* out) {
+  if (!C.bbox_part) C.bbox_part = C.alloc<double>(6 * kMaxPartials);
   int nb = std::min(red_grid(C.nsv), kMaxPartials);
   k_sv_bbox<<<nb, kBlock, 0, C.stream>>>(contactdev(C), x, C.bbox_part);
   C.check_launch();
-  k_bbox_final<<<1, kBlock, 0, C.stream>>>(C.bbox_part, nb, C.bbox_res);
+  k_bbox_final<<<1, kBlock, 0, C.stream>>>(C.bbox_part, nb, out);
   C.check_launch();
-  double bb[6];
-  JGS2_CUDA(cudaMemcpyAsync(bb, C.bbox_res, sizeof(bb), cudaMemcpyDeviceToHost, C.stream));
+}
+
+// bounding box on the host: bb[6] = (min xyz, -max xyz)
+inline void hier_bbox(Ctx& C, const double* x, double* bb) {
+  if (!C.bbox_res) C.bbox_res = C.alloc<double>(6);
+  hier_bbox_launch(C, x, C.bbox_res);
+  JGS2_CUDA(cudaMemcpyAsync(bb, C.bbox_res, 6 * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
   C.sync();
+}
+
+// level-0 cell and the dense per-level grids over the bounding box bb
+// (any box is correct: cell coordinates are clamped; it only sets the
+// resolution)
+inline void hier_geometry(Ctx& C, const double* bb, HierArgs& a) {
   double ext[3], emax = 0.0;
   for (int k = 0; k < 3; ++k) {
     double lo = bb[k], hi = -bb[3 + k];
-    if (!std::isfinite(lo) || !std::isfinite(hi) || hi < lo) lo = hi = 0.0;  // clamping keeps any box correct
+    if (!std::isfinite(lo) || !std::isfinite(hi) || hi < lo) lo = hi = 0.0;
     a.g.org[k] = lo;
     ext[k] = hi - lo;
     emax = std::max(emax, ext[k]);
@@ -406,9 +415,9 @@ inline long long scan_counts(Ctx& C, long long* cnt, long long* off, long long n
 }
 
 // geometry, levels, both grids (one sorted list) and the cell directory for
-// radii b * s + pad. Two host syncs (bounding box, entry count).
-inline void hier_prepare(Ctx& C, HierArgs& a, const double* x) {
-  hier_geometry(C, x, a);
+// radii b * s + pad. One host sync (the entry count).
+inline void hier_prepare(Ctx& C, HierArgs& a, const double* bb) {
+  hier_geometry(C, bb, a);
   HierList& h = C.hier;
   int nobj = C.nsv + C.nst;
   if (!C.hier_lev) {
@@ -459,7 +468,7 @@ inline void hier_prepare(Ctx& C, HierArgs& a, const double* x) {
 
 // min over cross-body pairs of dist / rate among the pairs with rate < b
 // (those whose boxes of radius b s overlap); INFINITY if there are none
-inline double hier_min_ratio(Ctx& C, const double* x, const double* dx, double b) {
+inline double hier_min_ratio(Ctx& C, const double* x, const double* dx, double b, const double* bb) {
   HierArgs a;
   a.cd = contactdev(C);
   a.x = x;
@@ -476,7 +485,7 @@ inline double hier_min_ratio(Ctx& C, const double* x, const double* dx, double b
     a.stats = st;
   }
   auto t0 = now();
-  hier_prepare(C, a, x);
+  hier_prepare(C, a, bb);
   auto t1 = now();
   const HierList& h = C.hier;
   double m = INFINITY;
@@ -509,19 +518,13 @@ inline double hier_min_ratio(Ctx& C, const double* x, const double* dx, double b
 // one has the exact minimum. Steps can be huge (the exact collect spreads
 // barrier forces over whole bodies), and the limiting pair is then found
 // with small boxes instead of body-sized ones.
-inline double hier_cap_min(Ctx& C, const double* x, const double* dx, double cap_ub) {
+inline double hier_cap_min(Ctx& C, const double* x, const double* dx, double cap_ub, double smax,
+                           const double* bb) {
   double bmax = cap_ub / 0.9 * (1.0 + 1e-6);
-  ContactDev cd = contactdev(C);
-  k_sv_maxstep<<<red_grid(C.nsv), kBlock, 0, C.stream>>>(cd, dx, C.partials + R_AUX * kMaxPartials,
-                                                         C.counters + R_AUX, C.res + R_AUX);
-  C.check_launch();
-  double smax = 0.0;
-  JGS2_CUDA(cudaMemcpyAsync(&smax, C.res + R_AUX, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
-  C.sync();
   if (!(smax > 0.0)) return INFINITY;  // nothing moves: no pair lowers the cap
   double b = std::isfinite(smax) ? std::min(bmax, 2.0 * C.grid_cell / smax) : bmax;
   for (;;) {
-    double m = hier_min_ratio(C, x, dx, b);
+    double m = hier_min_ratio(C, x, dx, b, bb);
     if (m < b || b >= bmax) return m;
     b = std::min(bmax, 4.0 * b);
   }
@@ -530,7 +533,8 @@ inline double hier_cap_min(Ctx& C, const double* x, const double* dx, double cap
 // Cross-body (vertex, triangle) pairs that can be within dhat at some
 // x + gamma dx, gamma <= gmax, each exactly once, into (cv, ct). Returns the
 // count, or -1 (nothing written) when it exceeds `budget`.
-inline long long hier_candidates(Ctx& C, const double* x, const double* dx, double gmax, long long budget) {
+inline long long hier_candidates(Ctx& C, const double* x, const double* dx, double gmax, long long budget,
+                                 const double* bb_in = nullptr) {
   HierArgs a;
   a.cd = contactdev(C);
   a.x = x;
@@ -538,7 +542,10 @@ inline long long hier_candidates(Ctx& C, const double* x, const double* dx, doub
   a.b = gmax * (1.0 + 1e-6);
   a.pad = 0.5 * C.dhat * (1.0 + 1e-6);
   a.dlim = 2.0 * a.pad;
-  hier_prepare(C, a, x);
+  double bb[6];
+  if (bb_in) memcpy(bb, bb_in, sizeof(bb));
+  else hier_bbox(C, x, bb);
+  hier_prepare(C, a, bb);
   const HierList& h = C.hier;
   int nobj = C.nsv + C.nst;
   if (!C.cand_cnt) {

@@ -199,10 +199,10 @@ void local_systems(Ctx& C, double* A_out, double* g_out, double* corr_out) {
 // x + gamma dx, gamma <= gmax (see trials.cuh).
 constexpr long long kCandBudget = 1LL << 26;
 
-void trial_candidates(Ctx& C, double gmax) {
+void trial_candidates(Ctx& C, double gmax, const double* bb = nullptr) {
   C.ncand = 0;
   if (!contact_active(C) || !use_tri_grid(C)) return;
-  long long n = hier_candidates(C, C.x, C.dx, gmax, kCandBudget);
+  long long n = hier_candidates(C, C.x, C.dx, gmax, kCandBudget, bb);
   C.ncand = n < 0 ? -1 : (int)n;  // -1: a huge step, exact per-trial detection
 }
 
@@ -316,15 +316,18 @@ void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
     // global backtracking (local_solver.py:555-577), trials in batches
     bool cap_needed = contact_active(C) && (C.npairs > 0 || C.nplanes > 0);
     double cap = 1.0;
+    double bb[6];
+    bool have_bb = false;
     if (cap_needed) {
       C.phase_begin(8, 0.0);
-      cap = contact_step_cap(C, C.x, C.dx, true);
+      cap = contact_step_cap(C, C.x, C.dx, true, bb);
+      have_bb = use_tri_grid(C);
       C.phase_end();
     }
     JGS2_CUDA(cudaMemcpyAsync(&acts_ls, C.ls_final + 2, sizeof(int), cudaMemcpyDeviceToHost, C.stream));
     if (contact_active(C)) {
       C.phase_begin(9, 0.0);
-      trial_candidates(C, cap);
+      trial_candidates(C, cap, have_bb ? bb : nullptr);
       C.phase_end();
     }
     const int MH = C.max_halvings;
