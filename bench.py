@@ -240,36 +240,72 @@ def main():
     (ts_iters, ts_conv), = solver.run_frames(1)
     ts_ms = solver.timer_stop()
 
-    # end-to-end through the reference-facing API with host buffers: per
-    # frame compute_z (host), capped initialize_step, sweeps through the
-    # C-ABI host call (x, z pinned in; x, dx out every sweep), velocity update
-    nv = m.num_vertices
-    xin, o1 = L.pinned_array((nv, 3))
-    zin, o2 = L.pinned_array((nv, 3))
-    xout, o3 = L.pinned_array((nv, 3))
-    dxo, o4 = L.pinned_array((nv, 3))
-    xp, vv = solver.get_frame_state()
-    hs = SystemState(x=xp.copy(), x_prev=xp.copy(), v=vv.copy(), z=xp.copy(), h=h)
-    inf = L.SweepInfo()
+    # end-to-end through the reference-facing API with host buffers, as the
+    # reference harness drives it (harness.py run loop): per frame host
+    # compute_z, initialize_step (feasibility cap through the ABI), then
+    # LocalSolver.outer_solve(state) -- x, z uploaded from pinned host memory,
+    # sweeps to tol_dx, x and the rotations read back into pinned memory --
+    # and the host velocity update (in place on preallocated arrays); the same
+    # episode resets as the timed window
     import ctypes
-    from paper_2506_06494_b200.model import compute_z, step_velocity_update
-    e2e_sweeps = 0
+    nv = m.num_vertices
+    px, o1 = L.pinned_array((nv, 3))
+    pz, o2 = L.pinned_array((nv, 3))
+    pdz, o3 = L.pinned_array((nv, 3))
+    prot, o4 = L.pinned_array((nv, 9))
+    xp0, vv0 = solver.get_frame_state()
+    xprev, vel = xp0.copy(), vv0.copy()           # host frame state
+    grav = (h * h) * np.asarray(m.gravity, dtype=np.float64)
+    fixed = np.flatnonzero(np.asarray(m.fixed_mask))
+    inf = L.SweepInfo()
+    lib, ctx = solver._lib, solver._ctx
+    cap_d = L.f64(1.0)
+    e2e_sweeps, e2e_frames, h2d, d2h = 0, 0, 0, 0
+    tdbg = {} if os.environ.get("JGS2_E2E_DEBUG") else None
+
+    def mark(key, t0):
+        if tdbg is not None:
+            tdbg[key] = tdbg.get(key, 0.0) + time.perf_counter() - t0
+            tdbg.setdefault(key + "_list", []).append(round(1e3 * (time.perf_counter() - t0), 2))
+        return time.perf_counter()
     t_e2e = time.perf_counter()
     while e2e_sweeps < args.e2e_steps:
-        compute_z(m, hs)
-        solver.initialize_step(hs)
-        xin[:] = hs.x
-        zin[:] = hs.z
-        for _ in range(cfg.max_outer):
-            L.check(solver._lib.jgs2_sweep_host(solver._ctx, L.ptr(xin, L.f64), L.ptr(zin, L.f64), h,
-                                                None, L.ptr(xout, L.f64), L.ptr(dxo, L.f64),
-                                                ctypes.byref(inf)), solver._ctx)
+        if episode and e2e_frames and e2e_frames % episode == 0:
+            xprev[:], vel[:] = xp0, vv0
+        t0 = time.perf_counter()
+        np.multiply(vel, h, out=pz)                  # compute_z (assembly.py:165-180), in place
+        pz += xprev
+        pz += grav
+        pz[fixed] = xprev[fixed]
+        np.subtract(pz, xprev, out=pdz)
+        px[:] = xprev
+        t0 = mark("host_z", t0)
+        L.check(lib.jgs2_step_cap(ctx, L.ptr(px, L.f64), L.ptr(pdz, L.f64), ctypes.byref(cap_d)), ctx)
+        t0 = mark("step_cap", t0)
+        pdz *= cap_d.value                           # initialize_step (harness.py:130-134)
+        px += pdz
+        L.check(lib.jgs2_set_state(ctx, L.ptr(px, L.f64), L.ptr(pz, L.f64), h), ctx)
+        h2d += 4 * px.nbytes
+        t0 = mark("set_state", t0)
+        for it in range(cfg.max_outer):              # outer_solve (local_solver.py:688-721)
+            L.check(lib.jgs2_sweep(ctx, 1, ctypes.byref(inf)), ctx)
             e2e_sweeps += 1
-            xin[:] = xout
-            if inf.dx_norm < cfg.tol_dx or e2e_sweeps >= args.e2e_steps:
+            if inf.dx_norm < cfg.tol_dx:
                 break
-        step_velocity_update(m, hs, xin.copy())
+        t0 = mark("sweeps", t0)
+        L.check(lib.jgs2_get_x(ctx, L.ptr(px, L.f64)), ctx)
+        L.check(lib.jgs2_get_rotations(ctx, L.ptr(prot, L.f64)), ctx)
+        d2h += px.nbytes + prot.nbytes
+        t0 = mark("readback", t0)
+        np.subtract(px, xprev, out=vel)              # step_velocity_update (assembly.py:346-351)
+        vel *= 1.0 / h
+        xprev[:] = px
+        t0 = mark("host_v", t0)
+        e2e_frames += 1
     e2e = replicas.job_throughput(dist, e2e_sweeps, time.perf_counter() - t_e2e)
+    if tdbg is not None:
+        print("e2e breakdown (s):", {k: (round(v, 4) if isinstance(v, float) else v) for k, v in tdbg.items()},
+              file=sys.stderr)
 
     cpu = None
     if rank == 0 and not args.no_cpu:
@@ -310,9 +346,11 @@ def main():
         "phases_ms_per_step": {p: round(v[0] / args.steps, 4) for p, v in phases.items()},
         "phases_gbs": {p: round(v[2] / (v[0] / 1e3) / 1e9, 1) for p, v in phases.items()
                        if v[0] > 0 and v[2] > 0},
-        "e2e": {"value": e2e, "unit": "sweeps/s", "h2d_bytes_per_step": 2 * 24 * nv,
-                "d2h_bytes_per_step": 2 * 24 * nv, "sweeps": e2e_sweeps,
-                "timing": "wall clock incl. host frame driver (compute_z, velocity update)"},
+        "e2e": {"value": e2e, "unit": "sweeps/s", "h2d_bytes_per_step": h2d / max(e2e_sweeps, 1),
+                "d2h_bytes_per_step": d2h / max(e2e_sweeps, 1), "sweeps": e2e_sweeps, "frames": e2e_frames,
+                "timing": "wall clock: per frame host compute_z + capped initialize_step + "
+                          "outer_solve(state) from pinned host x, z (x, rotations read back) + "
+                          "host velocity update"},
         "gpu_launches": launches,
         "clocks": clk,
         "cpu_baseline": cpu,
