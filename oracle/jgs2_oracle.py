@@ -555,6 +555,7 @@ class OracleConfig:
     track_energy: bool = True
     max_halvings: int = 30
     alpha_floor: float = 1e-6
+    mode: str = "jacobi"          # or "gauss_seidel" (local_solver.py:627-649)
 
 
 @dataclass
@@ -675,15 +676,17 @@ class OracleSolver:
                     own = gp[3 * pos:3 * pos + 3]
                 g[kk] += rows.T @ gp - own
 
-    def reduced_systems(self, x, z, h, verts, g_asm, pairs, rot):
-        """Frozen Schur block + sampled correction (local_solver.py:392-416)."""
+    def reduced_systems(self, x, z, h, verts, g_asm, pairs, rot, q=None, corr=None):
+        """Frozen Schur block + sampled correction (local_solver.py:392-416);
+        q / corr given: the sweep-start collect and corrections (GS colours)."""
         p, m = self.p, self.m
         ri = rot[verts]
         a = -np.einsum("vab,vbc,vdc->vad", ri, p.gbar[verts], ri)
-        q = self.collect(rot, g_asm)
+        if q is None:
+            q = self.collect(rot, g_asm)
         qg = q[p.group[verts]].reshape(verts.size, -1)
         g = -np.einsum("vab,vbk,vk->va", ri, p.gbar_rows[verts], qg)
-        a = a + self.corrections(x, verts, rot)
+        a = a + (self.corrections(x, verts, rot) if corr is None else corr)
         a = 0.5 * (a + np.swapaxes(a, 1, 2))
         wmin = np.linalg.eigvalsh(a).min(axis=1)
         bad = wmin <= 0.0
@@ -779,7 +782,8 @@ class OracleSolver:
         return x0 + gamma * dx, gamma * dx, halv
 
     def sweep(self, state, rot):
-        """One Jacobi outer iteration; mutates state.x (local_solver.py:606-655)."""
+        """One outer iteration (Jacobi or Gauss-Seidel); mutates state.x
+        (local_solver.py:606-655)."""
         m, p = self.m, self.p
         x, z, h = state.x, state.z, state.h
         pairs = find_pairs(m, x)
@@ -788,15 +792,36 @@ class OracleSolver:
         guard = self.cfg.local_line_search
         e0 = total_energy(m, z, h, x, pairs) if guard else None
         verts = p.free
-        g_asm = self.assembled_field(x, z, h, pairs)
-        a, g = self.reduced_systems(x, z, h, verts, g_asm, pairs, rot)
-        delta = self.solve3(a, -g)
-        alpha, acts = self.line_search(x, verts, delta, pairs, a, g)
-        info["line_search_activations"] += acts
-        info["grad_sq"] += float(np.sum(g_asm[~np.asarray(m.fixed_mask)] ** 2))
         dx = np.zeros_like(x)
-        dx[verts] = alpha[:, None] * delta
-        state.x = x + dx
+        if self.cfg.mode == "jacobi":
+            g_asm = self.assembled_field(x, z, h, pairs)
+            a, g = self.reduced_systems(x, z, h, verts, g_asm, pairs, rot)
+            delta = self.solve3(a, -g)
+            alpha, acts = self.line_search(x, verts, delta, pairs, a, g)
+            info["line_search_activations"] += acts
+            info["grad_sq"] += float(np.sum(g_asm[~np.asarray(m.fixed_mask)] ** 2))
+            dx[verts] = alpha[:, None] * delta
+            state.x = x + dx
+        else:
+            # Gauss-Seidel (local_solver.py:627-649): collect and corrections
+            # at the sweep start; per colour (ascending) pairs, assembled field,
+            # reduced systems and local search at the current positions
+            x_cur = x.copy()
+            q0 = self.collect(rot, self.assembled_field(x, z, h, pairs))
+            groups = self.color_groups()
+            corr0 = [self.corrections(x, cv, rot) for cv in groups]
+            for cv, c0 in zip(groups, corr0):
+                cpairs = find_pairs(m, x_cur)
+                g_asm = self.assembled_field(x_cur, z, h, cpairs)
+                a, g = self.reduced_systems(x_cur, z, h, cv, g_asm, cpairs, rot, q=q0, corr=c0)
+                delta = self.solve3(a, -g)
+                alpha, acts = self.line_search(x_cur, cv, delta, cpairs, a, g)
+                info["line_search_activations"] += acts
+                info["grad_sq"] += float(np.sum(g_asm[cv] ** 2))
+                step = alpha[:, None] * delta
+                x_cur[cv] += step
+                dx[cv] += step
+            state.x = x_cur
         info["grad_norm"] = np.sqrt(info["grad_sq"])
         self.pairs = pairs
         if guard:
@@ -804,6 +829,14 @@ class OracleSolver:
             info["line_search_activations"] += halv
         info["max_local_step"] = float(np.linalg.norm(dx, axis=1).max(initial=0.0))
         return dx, info
+
+    def color_groups(self):
+        """Free vertices per colour, colours ascending (local_solver.py:298-303)."""
+        colors = np.asarray(self.m.colors)
+        free = ~np.asarray(self.m.fixed_mask)
+        ncol = int(colors.max()) + 1 if colors.size else 0
+        out = [np.flatnonzero((colors == c) & free) for c in range(ncol)]
+        return [g for g in out if g.size]
 
     def outer_solve(self, state):
         """local_solver.py:688-721."""

@@ -158,8 +158,42 @@ def incidence_csr(tets, nv):
     return ptr, (order // 4).astype(np.int64), (order % 4).astype(np.int64)
 
 
+def greedy_color(tets, nv):
+    """First-fit greedy vertex colouring in ascending vertex id: two vertices
+    sharing a tet never share a colour (mesh.py:164-178, same order and rule,
+    so the colour groups of the Gauss-Seidel schedule are identical)."""
+    tets = np.asarray(tets, dtype=np.int64)
+    # vertex adjacency (CSR, neighbours through shared tets)
+    a = np.repeat(tets, 4, axis=1).ravel()
+    b = np.tile(tets, (1, 4)).ravel()
+    keep = a != b
+    a, b = a[keep], b[keep]
+    order = np.lexsort((b, a))
+    a, b = a[order], b[order]
+    uniq = np.ones(a.size, dtype=bool)
+    uniq[1:] = (a[1:] != a[:-1]) | (b[1:] != b[:-1])
+    a, b = a[uniq], b[uniq]
+    ptr = np.zeros(nv + 1, dtype=np.int64)
+    np.cumsum(np.bincount(a, minlength=nv), out=ptr[1:])
+    colors = np.full(nv, -1, dtype=np.int64)
+    for j in range(nv):
+        nb = colors[b[ptr[j]:ptr[j + 1]]]
+        used = np.zeros(nb.size + 2, dtype=bool)
+        nb = nb[(nb >= 0) & (nb < used.size)]
+        used[nb] = True
+        colors[j] = int(np.argmin(used))
+    return colors
+
+
 class Model:
     """Concatenated multi-body scene (assembly.py:40-116)."""
+
+    @property
+    def colors(self):
+        """Greedy vertex colouring (assembly.py:110), computed on first use."""
+        if getattr(self, "_colors", None) is None:
+            self._colors = greedy_color(self.tets, self.num_vertices)
+        return self._colors
 
     def __init__(self, bodies, gravity=(0.0, -9.8, 0.0), planes=(), barrier=None):
         self.bodies = []
@@ -233,6 +267,7 @@ class Model:
         self.planes = [HalfSpace(p, n) for p, n in zip(a["plane_points"], a["plane_normals"])]
         self.barrier = BarrierParams(*map(float, a["barrier"])) if a["barrier"].size else None
         self.bodies = list(a["body_vertex_offsets"])
+        self._colors = np.array(a["colors"]) if "colors" in a else None
         self._finish()
         return self
 

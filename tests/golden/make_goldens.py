@@ -223,7 +223,17 @@ def c1_scene():
 
 # (frame, sweep) of the per-kernel snapshot: a deformed state, in contact
 # for the contact scenes.
-SNAPSHOT = {"cube_drop": (20, 2), "two_body": (25, 2)}
+SNAPSHOT = {"cube_drop": (20, 2), "two_body": (25, 2), "cube_drop_gs": (20, 2), "two_body_gs": (25, 2)}
+
+
+def gauss_seidel(make):
+    """The same scene with scene.solver.mode = "gauss_seidel" (colour sweeps,
+    local_solver.py:627-649); the precompute stays per-vertex (harness.py:66-69)."""
+    def build():
+        scene, model, frames = make()
+        scene.solver.mode = "gauss_seidel"
+        return scene, model, frames
+    return build
 
 SCENES = {
     "beam": lambda: scene_from_toml("beam"),
@@ -231,6 +241,9 @@ SCENES = {
     "cube_drop": lambda: scene_from_toml("cube_drop"),
     "two_body": lambda: scene_from_toml("two_body"),
     "c1": lambda: (*c1_scene(), 3),
+    "beam_gs": gauss_seidel(lambda: scene_from_toml("beam", frames=3)),
+    "cube_drop_gs": gauss_seidel(lambda: scene_from_toml("cube_drop", frames=24)),
+    "two_body_gs": gauss_seidel(lambda: scene_from_toml("two_body", frames=28)),
 }
 
 

@@ -75,3 +75,30 @@ def test_barrier_known_answer():
     # test_energy.py:132-136 known value at d=0.5, dhat=kappa=1
     b, _, _ = orc.barrier(0.5, 1.0, 1.0)
     assert b == pytest.approx(0.17328679513998632, rel=1e-15)
+
+
+GS_SCENES = ("beam_gs", "cube_drop_gs", "two_body_gs")
+
+
+@pytest.mark.parametrize("name", GS_SCENES)
+def test_oracle_gauss_seidel_trajectory_matches_reference(golden, name):
+    # scene.solver.mode = "gauss_seidel" goldens (local_solver.py:627-649)
+    g = golden(name)
+    model, solver, h = make_solver(g)
+    solver.cfg.mode = "gauss_seidel"
+
+    def sweep(state):
+        rot = orc.vertex_rotations(model, state.x)
+        return solver.sweep(state, rot)
+
+    rep = replay(g, sweep, lambda x: orc.find_pairs(model, x).as_rows())
+    assert rep["iters"] == rep["iters_ref"]
+    assert rep["pair_mismatch"] == 0
+    assert rep["pos"] < 1e-9, rep
+
+
+def test_gauss_seidel_equals_jacobi_without_contact(golden):
+    # bitwise equal to Jacobi when there is no contact
+    gs, jac = golden("beam_gs"), golden("beam")
+    n = gs["traj_x"].shape[0]
+    assert np.array_equal(gs["traj_x"], jac["traj_x"][:n])
