@@ -83,6 +83,8 @@ typedef struct jgs2_config {
   int32_t track_energy;
   int32_t max_halvings;
   double alpha_floor;
+  int32_t mode;            /* 0 jacobi, 1 gauss_seidel (local_solver.py:627-649) */
+  int32_t pad_;
 } jgs2_config;
 
 /* sweep() info dict (local_solver.py:613-614, 654) + extras. */
@@ -117,6 +119,10 @@ int32_t jgs2_device_count(void);
 /* ---- setup (LocalSolver.__init__, local_solver.py:217-240) ------------ */
 int32_t jgs2_set_model(jgs2_ctx* ctx, const jgs2_model* model);
 int32_t jgs2_set_precompute(jgs2_ctx* ctx, const jgs2_precompute* pre, const jgs2_config* cfg);
+/* Vertex colours for the Gauss-Seidel schedule (Model.colors, greedy
+ * first-fit in ascending vertex id, mesh.py:164-178; nv entries): free
+ * vertices are updated colour by colour, ascending (local_solver.py:298-303). */
+int32_t jgs2_set_colors(jgs2_ctx* ctx, const int64_t* colors);
 /* Rest Hessian M/h^2 + PSD elastic, Dirichlet-eliminated, factored on the
  * device (replaces subspace.rest_factorization, subspace.py:126-130). */
 int32_t jgs2_factor_rest(jgs2_ctx* ctx, double h_ref, int32_t leaf_size, jgs2_factor_info* info);

@@ -17,7 +17,7 @@ P = C.POINTER
 EXPORTS = (
     "jgs2_create", "jgs2_destroy", "jgs2_last_error", "jgs2_device_count",
     "jgs2_set_model", "jgs2_set_precompute", "jgs2_factor_rest", "jgs2_factor_blocks",
-    "jgs2_set_state", "jgs2_set_x", "jgs2_get_x", "jgs2_get_dx", "jgs2_set_rotations",
+    "jgs2_set_colors", "jgs2_set_state", "jgs2_set_x", "jgs2_get_x", "jgs2_get_dx", "jgs2_set_rotations",
     "jgs2_get_rotations", "jgs2_rotations", "jgs2_sweep", "jgs2_sweep_host",
     "jgs2_outer_solve", "jgs2_total_energy", "jgs2_assembled_field", "jgs2_reduced_collect",
     "jgs2_sampled_corrections", "jgs2_reduced_systems", "jgs2_find_pairs",
@@ -69,7 +69,8 @@ class Precompute(C.Structure):
 
 class Config(C.Structure):
     _fields_ = [("tol_dx", f64), ("max_outer", i32), ("local_line_search", i32),
-                ("track_energy", i32), ("max_halvings", i32), ("alpha_floor", f64)]
+                ("track_energy", i32), ("max_halvings", i32), ("alpha_floor", f64),
+                ("mode", i32), ("pad_", i32)]
 
 
 class SweepInfo(C.Structure):
@@ -105,6 +106,7 @@ def lib():
         "jgs2_set_precompute": (i32, [vp, P(Precompute), P(Config)]),
         "jgs2_factor_rest": (i32, [vp, f64, i32, P(FactorInfo)]),
         "jgs2_factor_blocks": (i32, [vp, i64, P(i64), P(i64), P(f64), i32, P(FactorInfo)]),
+        "jgs2_set_colors": (i32, [vp, P(i64)]),
         "jgs2_set_state": (i32, [vp, P(f64), P(f64), f64]),
         "jgs2_set_x": (i32, [vp, P(f64)]),
         "jgs2_get_x": (i32, [vp, P(f64)]),

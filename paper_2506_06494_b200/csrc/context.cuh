@@ -126,6 +126,12 @@ struct Ctx {
   double tol_dx = 1e-3, alpha_floor = 1e-6;
   int max_outer = 500, max_halvings = 30;
   bool local_line_search = true, track_energy = true;
+  int mode = 0;                // 0 jacobi, 1 gauss_seidel
+  // Gauss-Seidel colour groups: free vertices by colour (ascending id)
+  std::vector<int> color_ptr;
+  int* color_verts = nullptr;
+  double* x0 = nullptr;        // sweep-start positions (GS)
+  double* gs_gsq = nullptr;    // per-colour grad_sq (device)
 
   // static device data
   int4* tets = nullptr;

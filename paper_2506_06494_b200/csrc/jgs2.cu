@@ -177,10 +177,18 @@ void hessians_join(Ctx& C) {
   C.hess_pending = false;
 }
 
-void local_systems(Ctx& C, double* A_out, double* g_out, double* corr_out) {
+// Local systems of the free vertices, or of the vertices in `list` (a
+// Gauss-Seidel colour; the element Hessians are then already in place).
+void local_systems(Ctx& C, double* A_out, double* g_out, double* corr_out, const int* list = nullptr,
+                   int nlist = 0) {
   DevModel m = devmodel(C);
-  hessians_async(C);  // no-op if already in flight
-  hessians_join(C);
+  if (list) {
+    m.nfree = nlist;
+    m.free_list = list;
+  } else {
+    hessians_async(C);  // no-op if already in flight
+    hessians_join(C);
+  }
   C.phase_begin(4, bytes_local(C));
   JGS2_CUDA(cudaMemsetAsync(C.ls_cnt, 0, (C.max_halvings + 2) * sizeof(int), C.stream));
   JGS2_CUDA(cudaMemsetAsync(C.ls_max, 0, (C.max_halvings + 2) * sizeof(unsigned long long), C.stream));
@@ -190,7 +198,7 @@ void local_systems(Ctx& C, double* A_out, double* g_out, double* corr_out) {
   a.x = C.x; a.pairs = C.pairs; a.pair_g = C.pair_g; a.pair_h = C.pair_h;
   a.vp_ptr = C.vp_ptr; a.vp_list = C.vp_list; a.planes = C.planes;
   a.vr_ptr = C.vr_ptr; a.vr_keys = C.vr_keys; a.vr_rows = C.vr_rows;
-  k_local<<<grid_for(C.nfree, 128), 128, 0, C.stream>>>(m, a);
+  if (m.nfree > 0) k_local<<<grid_for(m.nfree, 128), 128, 0, C.stream>>>(m, a);
   C.check_launch();
   C.phase_end();
 }
@@ -272,6 +280,113 @@ void trial_energies(Ctx& C, const double* gam, int n, double* E, bool* infeasibl
   }
 }
 
+// ---- Gauss-Seidel colour updates (local_solver.py:627-649)
+// sum of g_asm^2 over a colour's vertices (deterministic two-level reduction)
+__global__ void k_sumsq_list(const int* list, int n, const double* g, double* partials, unsigned* counter,
+                             double* out) {
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int v = list[i];
+    acc += g[3 * v] * g[3 * v] + g[3 * v + 1] * g[3 * v + 1] + g[3 * v + 2] * g[3 * v + 2];
+  }
+  grid_reduce<OP_SUM>(acc, partials, counter, out);
+}
+
+// step = alpha delta for a colour's vertices (k_apply_alpha's rule); x += step, dx += step
+__global__ void k_apply_list(const int* list, int n, const double* delta, const double* alpha0, const int* kacc,
+                             const int* lsf, int line_search, int max_halvings, double alpha_floor, double* x,
+                             double* dx) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int v = list[i];
+  double al = 1.0;
+  if (line_search) {
+    int T = lsf[0], fl = lsf[1];
+    int kv = kacc[v];
+    al = alpha0[v];
+    if (kv <= T) {
+      for (int it = 0; it < kv; ++it) al *= 0.5;
+    } else if (fl) {
+      al = alpha_floor;
+    } else {
+      for (int it = 0; it <= max_halvings; ++it) al *= 0.5;
+    }
+  }
+  for (int c = 0; c < 3; ++c) {
+    double st = al * delta[3 * v + c];
+    x[3 * v + c] += st;
+    dx[3 * v + c] += st;
+  }
+}
+
+// Colour sweeps: q0 (collect) and the element Hessians (corrections) at the
+// sweep start; per colour ascending, pairs + assembled field at the current
+// positions, local systems with q0 / corrections, the colour's local search,
+// x += step. Leaves C.x = x0 (sweep start) and C.dx = the summed steps for
+// the global backtracking. Returns sum of grad_sq; acts += activations.
+double gauss_seidel_colours(Ctx& C, int* acts) {
+  bool guard = C.local_line_search;
+  size_t bytes = 3 * (size_t)C.nv * sizeof(double);
+  hessians_async(C);
+  hessians_join(C);
+  if (!C.x0) {
+    C.x0 = C.alloc<double>(3 * (size_t)C.nv);
+    C.gs_gsq = C.alloc<double>(std::max<size_t>(C.color_ptr.size(), 1));
+  }
+  JGS2_CUDA(cudaMemcpyAsync(C.x0, C.x, bytes, cudaMemcpyDeviceToDevice, C.stream));
+  JGS2_CUDA(cudaMemsetAsync(C.dx, 0, bytes, C.stream));
+  int nc = (int)C.color_ptr.size() - 1;
+  std::vector<int> act(std::max(nc, 1), 0);
+  int* hacts = reinterpret_cast<int*>(C.h_res + 32);  // pinned scratch (<= 32 colours per chunk)
+  for (int c = 0; c < nc; ++c) {
+    const int* list = C.color_verts + C.color_ptr[c];
+    int n = C.color_ptr[c + 1] - C.color_ptr[c];
+    if (n == 0) continue;
+    if (c > 0) {  // positions moved: pairs and assembled field at the current x
+      if (contact_active(C)) {
+        C.phase_begin(7, 0.0);
+        contact_find_pairs(C, C.x, nullptr, 0.0);
+        C.phase_end();
+        if (contact_infeasible(C)) throw Error(JGS2_E_INFEASIBLE, "barrier distance <= 0 during a colour sweep");
+      }
+      vertex_pass(C, false);
+      if (contact_active(C)) {
+        C.phase_begin(7, 0.0);
+        contact_add_gradients(C);
+        C.phase_end();
+      }
+    }
+    k_sumsq_list<<<std::min(red_grid(n), 256), kBlock, 0, C.stream>>>(
+        list, n, C.gasm, C.partials + R_AUX * kMaxPartials, C.counters + R_AUX, C.gs_gsq + c);
+    C.check_launch();
+    local_systems(C, nullptr, nullptr, nullptr, list, n);
+    if (guard) {
+      k_ls_final<<<1, 1, 0, C.stream>>>(C.max_halvings, C.alpha_floor, C.ls_cnt, C.ls_max, C.ls_final);
+      C.check_launch();
+      JGS2_CUDA(cudaMemcpyAsync(hacts + (c % 32), C.ls_final + 2, sizeof(int), cudaMemcpyDeviceToHost, C.stream));
+    }
+    k_apply_list<<<grid_for(n), kBlock, 0, C.stream>>>(list, n, C.delta, C.alpha0, C.kacc, C.ls_final,
+                                                       guard ? 1 : 0, C.max_halvings, C.alpha_floor, C.x,
+                                                       C.dx);
+    C.check_launch();
+    if (guard && (c % 32 == 31 || c == nc - 1)) {
+      C.sync();
+      for (int k = c - (c % 32); k <= c; ++k) act[k] = hacts[k % 32];
+    }
+  }
+  std::vector<double> gsq(std::max(nc, 1), 0.0);
+  if (nc > 0)
+    JGS2_CUDA(cudaMemcpyAsync(gsq.data(), C.gs_gsq, nc * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+  JGS2_CUDA(cudaMemcpyAsync(C.x, C.x0, bytes, cudaMemcpyDeviceToDevice, C.stream));
+  C.sync();
+  double tot = 0.0;
+  for (int c = 0; c < nc; ++c) {
+    tot += gsq[c];
+    if (C.color_ptr[c + 1] > C.color_ptr[c]) *acts += act[c];
+  }
+  return tot;
+}
+
 // One sweep on the device state. rot: compute rotations at x (outer_solve);
 // otherwise use the context's current rotations.
 void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
@@ -296,35 +411,46 @@ void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
     C.phase_end();
   }
   collect(C);
-  local_systems(C, nullptr, nullptr, nullptr);
-  C.phase_begin(6, bytes_final(C));
-  if (guard) {
-    k_ls_final<<<1, 1, 0, C.stream>>>(C.max_halvings, C.alpha_floor, C.ls_cnt, C.ls_max, C.ls_final);
+  const int npairs_x = C.npairs;  // pairs at the sweep-start x
+  const bool gs = C.mode == 1 && C.color_ptr.size() > 1;
+  int gs_acts = 0;
+  double gs_gradsq = 0.0;
+  if (gs) {
+    gs_gradsq = gauss_seidel_colours(C, &gs_acts);
+  } else {
+    local_systems(C, nullptr, nullptr, nullptr);
+    C.phase_begin(6, bytes_final(C));
+    if (guard) {
+      k_ls_final<<<1, 1, 0, C.stream>>>(C.max_halvings, C.alpha_floor, C.ls_cnt, C.ls_max, C.ls_final);
+      C.check_launch();
+    }
+    k_apply_alpha<<<grid_for(C.nv), kBlock, 0, C.stream>>>(m, C.delta, C.alpha0, C.kacc, C.ls_final,
+                                                            guard ? 1 : 0, C.max_halvings,
+                                                            C.alpha_floor, C.dx);
     C.check_launch();
+    C.phase_end();
   }
-  k_apply_alpha<<<grid_for(C.nv), kBlock, 0, C.stream>>>(m, C.delta, C.alpha0, C.kacc, C.ls_final,
-                                                          guard ? 1 : 0, C.max_halvings,
-                                                          C.alpha_floor, C.dx);
-  C.check_launch();
-  C.phase_end();
   double gamma = 1.0, energy = 0.0;
   int halvings = 0;
   bool have_energy = false;
-  int pairs_at_start = C.npairs;
-  int acts_ls = 0;
+  int pairs_at_start = npairs_x;
+  int acts_ls = gs_acts;
   if (guard) {
     // global backtracking (local_solver.py:555-577), trials in batches
-    bool cap_needed = contact_active(C) && (C.npairs > 0 || C.nplanes > 0);
+    bool cap_needed = contact_active(C) && (npairs_x > 0 || C.nplanes > 0);
     double cap = 1.0;
     double bb[6];
     bool have_bb = false;
     if (cap_needed) {
       C.phase_begin(8, 0.0);
-      cap = contact_step_cap(C, C.x, C.dx, true, bb);
+      // the pair table bounds the cap only when it holds the pairs at x
+      // (after colour sweeps it holds the last colour's pairs)
+      cap = contact_step_cap(C, C.x, C.dx, !gs, bb);
       have_bb = use_tri_grid(C);
       C.phase_end();
     }
-    JGS2_CUDA(cudaMemcpyAsync(&acts_ls, C.ls_final + 2, sizeof(int), cudaMemcpyDeviceToHost, C.stream));
+    if (!gs)
+      JGS2_CUDA(cudaMemcpyAsync(&acts_ls, C.ls_final + 2, sizeof(int), cudaMemcpyDeviceToHost, C.stream));
     if (contact_active(C)) {
       C.phase_begin(9, 0.0);
       trial_candidates(C, cap, have_bb ? bb : nullptr);
@@ -404,8 +530,9 @@ void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
   if (info) {
     info->line_search_activations = guard ? acts_ls + halvings : 0;
     info->n_indefinite = n_indef;
-    info->grad_sq = C.h_res[R_GRADSQ];
-    info->grad_norm = std::sqrt(C.h_res[R_GRADSQ]);
+    double gsq = gs ? gs_gradsq : C.h_res[R_GRADSQ];
+    info->grad_sq = gsq;
+    info->grad_norm = std::sqrt(gsq);
     info->max_local_step = C.h_res[R_DXMAX];
     info->dx_norm = C.norm_scale * std::sqrt(C.h_res[R_DX2]);
     info->energy = energy;
@@ -541,6 +668,8 @@ int32_t jgs2_set_precompute(jgs2_ctx* ctx, const jgs2_precompute* p, const jgs2_
     C.track_energy = cfg->track_energy != 0;
     C.max_halvings = cfg->max_halvings;
     C.alpha_floor = cfg->alpha_floor;
+    if (cfg->mode != 0 && cfg->mode != 1) throw Error(JGS2_E_ARG, "mode must be 0 (jacobi) or 1 (gauss_seidel)");
+    C.mode = cfg->mode;
     if (C.tol_dx <= 0 || C.max_outer < 1 || C.max_halvings < 0)
       throw Error(JGS2_E_ARG, "invalid solver config");
     const int nv = C.nv;
@@ -665,6 +794,31 @@ int32_t jgs2_set_precompute(jgs2_ctx* ctx, const jgs2_precompute* p, const jgs2_
     }
     C.have_pre = true;
     C.sync();
+  });
+}
+
+int32_t jgs2_set_colors(jgs2_ctx* ctx, const int64_t* colors) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (!C.have_model) throw Error(JGS2_E_ARG, "model not set");
+    int64_t cmax = -1;
+    for (int v = 0; v < C.nv; ++v) {
+      if (colors[v] < 0) throw Error(JGS2_E_ARG, "negative colour");
+      cmax = std::max<int64_t>(cmax, colors[v]);
+    }
+    std::vector<int> cnt(cmax + 2, 0);
+    for (int v = 0; v < C.nv; ++v)
+      if (!C.h_fixed[v]) cnt[colors[v] + 1]++;
+    std::vector<int> ptr(1, 0);  // non-empty colour groups only (local_solver.py:298-303)
+    std::vector<int> verts;
+    for (int64_t c = 0; c <= cmax; ++c) {
+      if (cnt[c + 1] == 0) continue;
+      for (int v = 0; v < C.nv; ++v)
+        if (!C.h_fixed[v] && colors[v] == c) verts.push_back(v);
+      ptr.push_back((int)verts.size());
+    }
+    C.color_ptr = ptr;
+    C.color_verts = verts.empty() ? nullptr : C.upload(verts.data(), verts.size());
+    if (C.gs_gsq) C.gs_gsq = C.alloc<double>(std::max<size_t>(ptr.size(), 1));
   });
 }
 

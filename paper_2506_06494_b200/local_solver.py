@@ -10,9 +10,10 @@ IterationStats`` semantics (both mutate ``state.x``; ``outer_solve`` also sets
 fallback: a missing library or device raises ``RuntimeError``.
 
 Scope: ``subspace="corotated_cubature"`` with ``mode="jacobi"`` (the
-reference defaults). ``exact`` (a <=6000-DOF verification path) and ``none``
-(the plain VBD baseline) are out of scope and raise
-``ValueError``; Gauss-Seidel is SURVEY §8(f) "next".
+reference defaults) or ``mode="gauss_seidel"`` (colour sweeps,
+local_solver.py:627-649). ``exact`` (a <=6000-DOF verification path) and
+``none`` (the plain VBD baseline) are out of scope and raise
+``ValueError``.
 """
 
 import time
@@ -101,8 +102,6 @@ class LocalSolver:
         if config.subspace != "corotated_cubature":
             raise ValueError(f"subspace {config.subspace!r} is not on the GPU path "
                              "(only corotated_cubature; see SURVEY §2.1)")
-        if config.mode != "jacobi":
-            raise ValueError("the GPU path implements the Jacobi schedule")
         if precompute is None:
             if not bases:
                 raise ValueError("corotated_cubature needs precomputed bases")
@@ -206,7 +205,11 @@ class LocalSolver:
         c.track_energy = int(bool(cfg.track_energy))
         c.max_halvings = int(cfg.max_halvings)
         c.alpha_floor = float(cfg.alpha_floor)
+        c.mode = SCHEDULES.index(cfg.mode)
         self._call(self._lib.jgs2_set_precompute, C_ref(d), C_ref(c))
+        if cfg.mode == "gauss_seidel":  # colour groups (local_solver.py:298-303)
+            colors = L.i64a(self.model.colors)
+            self._call(self._lib.jgs2_set_colors, L.ptr(colors, L.i64))
 
     def close(self):
         if getattr(self, "_ctx", None):

@@ -16,19 +16,19 @@ pytestmark = pytest.mark.gpu
 ALL = SCENES_SMALL + ("c1",)
 
 
-def config_of(g):
+def config_of(g, mode="jacobi"):
     c = g["scene_cfg"]
     return SolverConfig(tol_dx=float(c[0]), max_outer=int(c[1]), max_halvings=int(c[2]),
                         alpha_floor=float(c[3]), local_line_search=bool(c[4]),
-                        track_energy=bool(c[5]))
+                        track_energy=bool(c[5]), mode=mode)
 
 
-def gpu_solver(g, matrix=True):
+def gpu_solver(g, matrix=True, mode="jacobi"):
     model, pre, h = scene_inputs(g)
     if matrix:   # the same Hbar the reference factored (subspace.rest_hessian)
-        return model, LocalSolver(model, config_of(g), precompute=pre,
+        return model, LocalSolver(model, config_of(g, mode), precompute=pre,
                                   hbar=orc.rest_hessian(model, h)), h
-    return model, LocalSolver(model, config_of(g), precompute=pre, h_ref=h), h
+    return model, LocalSolver(model, config_of(g, mode), precompute=pre, h_ref=h), h
 
 
 @pytest.mark.parametrize("name", ALL)
@@ -157,3 +157,41 @@ def test_device_frame_driver_matches_reference(golden, name):
         (it, conv), = s.run_frames(1)
         assert it == int(g["frame_iterations"][f]), (f, it)
         assert rel_err(s.get_x(), g["frame_x_final"][f]) < 1e-9
+
+
+@pytest.mark.parametrize("name", ("beam_gs", "cube_drop_gs", "two_body_gs"))
+def test_gauss_seidel_trajectory_matches_reference(golden, name):
+    # colour sweeps (local_solver.py:627-649) against the reference's own
+    # gauss_seidel trajectories: per-colour pair re-detection and local
+    # search, sweep-start collect and corrections
+    g = golden(name)
+    model, s, h = gpu_solver(g, mode="gauss_seidel")
+
+    def sweep(state):
+        return s.sweep(state, s.rotations(state.x))
+
+    rep = replay(g, sweep, s.find_pairs)
+    assert rep["pair_mismatch"] == 0, rep
+    assert rep["iters"] == rep["iters_ref"], rep
+    assert rep["pos"] < 1e-9, rep
+
+
+def test_gauss_seidel_contact_sweeps_match_oracle():
+    # ten-body contact scene (C4 construction at 6 cells/ball): GS sweeps
+    # against the oracle's GS on the same inputs
+    from paper_2506_06494_b200 import scenes
+    from paper_2506_06494_b200.precompute import Precompute
+    m, st, h, _ = scenes.build("c4s6")
+    pre = Precompute.injected(m, h, samples=6, seed=0)
+    cfg = SolverConfig(tol_dx=m.tol_dx, mode="gauss_seidel")
+    s = LocalSolver(m, cfg, precompute=pre, hbar=orc.rest_hessian(m, h))
+    o = orc.OracleSolver(m, pre, h, orc.OracleConfig(tol_dx=m.tol_dx, mode="gauss_seidel"))
+    from paper_2506_06494_b200.model import SystemState
+    sg = SystemState(x=st.x.copy(), x_prev=st.x_prev.copy(), v=st.v.copy(), z=st.z.copy(), h=h)
+    so = SystemState(x=st.x.copy(), x_prev=st.x_prev.copy(), v=st.v.copy(), z=st.z.copy(), h=h)
+    for _ in range(2):
+        rot = orc.vertex_rotations(m, so.x)
+        dxo, io = o.sweep(so, rot)
+        dxg, ig = s.sweep(sg, s.rotations(sg.x))
+        assert rel_err(sg.x, so.x) < 1e-9
+        assert ig["line_search_activations"] == io["line_search_activations"]
