@@ -253,7 +253,8 @@ def main():
     pz, o2 = L.pinned_array((nv, 3))
     pdz, o3 = L.pinned_array((nv, 3))
     prot, o4 = L.pinned_array((nv, 9))
-    xp0, vv0 = solver.get_frame_state()
+    # from the scene's initial state, like every episode of the timed window
+    xp0, vv0 = np.array(init.x_prev, dtype=np.float64), np.array(init.v, dtype=np.float64)
     xprev, vel = xp0.copy(), vv0.copy()           # host frame state
     grav = (h * h) * np.asarray(m.gravity, dtype=np.float64)
     fixed = np.flatnonzero(np.asarray(m.fixed_mask))
