@@ -195,3 +195,25 @@ def test_gauss_seidel_contact_sweeps_match_oracle():
         dxg, ig = s.sweep(sg, s.rotations(sg.x))
         assert rel_err(sg.x, so.x) < 1e-9
         assert ig["line_search_activations"] == io["line_search_activations"]
+
+
+def test_run_frames_from_reference_cache_matches_reference(golden, tmp_path):
+    # harness.run-style frames on the GPU solver, precompute loaded from the
+    # cache files the reference wrote; outputs in the reference's formats
+    from pathlib import Path
+    from paper_2506_06494_b200 import formats
+    from paper_2506_06494_b200.model import Model, SystemState
+    io = Path(__file__).resolve().parent / "golden" / "io"
+    g = golden("beam")
+    model = Model.from_arrays(g)
+    pre, info = formats.load_precompute_cache(io / "beam_bases.npz", io / "beam_cubature.npz")
+    h = float(g["scene_h"][0])
+    s = LocalSolver(model, config_of(g), precompute=pre, hbar=orc.rest_hessian(model, h))
+    state = SystemState.initial(model, h)
+    nf = int(g["frame_iterations"].size)
+    failed = formats.run_frames(model, s, state, nf, tmp_path)
+    assert failed == []
+    assert rel_err(state.x_prev, g["frame_x_final"][nf - 1]) < 1e-9
+    rows = formats.read_metrics(tmp_path / "metrics.csv")
+    assert len(rows) == int(g["frame_iterations"].sum())
+    assert (tmp_path / f"frame_{nf:04d}.obj").exists() and (tmp_path / f"body0_frame_{nf:04d}.node").exists()
