@@ -48,7 +48,7 @@ def build(force=False, verbose=False):
         return LIB
     LIBDIR.mkdir(exist_ok=True)
     libdir = cuda_lib_dir()
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = LIB.with_suffix(f".so.tmp{os.getpid()}")
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "-Xptxas", "-O3", "-I", str(PKG.parent / "include"),
            *[str(CSRC / s) for s in SOURCES], "-o", str(tmp),
