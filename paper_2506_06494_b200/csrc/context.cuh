@@ -63,7 +63,9 @@ struct HierList {
   long long *cnt = nullptr, *off = nullptr;
   unsigned *ka = nullptr, *kb = nullptr;  // dense cell index (all levels)
   int *ia = nullptr, *ib = nullptr;
-  int *cstart = nullptr, *cend = nullptr; // per-cell entry range [cstart, cend)
+  int *flag = nullptr, *rix = nullptr;    // run starts and their exclusive scan
+  int *run_begin = nullptr, *run_body = nullptr;  // body runs of the sorted entries
+  int *cstart = nullptr, *cend = nullptr; // per-cell run range [cstart, cend)
   long long ncells_cap = 0;
 };
 

@@ -197,13 +197,45 @@ __global__ void k_hier_entries(HierArgs a, const int* lev, const unsigned* masks
   if (!WRITE) cnt[o] = n;
 }
 
-// per-cell [start, end) of the sorted entries (cells without entries keep 0, 0)
-__global__ void k_hier_dir(const unsigned* keys, long long n, int* cstart, int* cend) {
+// Body runs of the sorted entries: a run is a maximal stretch of one cell
+// and one body (entries of a cell are in ascending object order, objects
+// numbered body by body). flag[i] = 1 where a run starts.
+__device__ __forceinline__ int entry_body(const ContactDev& cd, unsigned key, int id, unsigned ncells) {
+  return key >= ncells ? cd.vbody[cd.sv[id]] : cd.tbody[id];
+}
+__global__ void k_hier_run_flags(ContactDev cd, const unsigned* keys, const int* ids, long long n, unsigned ncells,
+                                 int* flag) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   unsigned k = keys[i];
-  if (i == 0 || keys[i - 1] != k) cstart[k] = (int)i;
-  if (i == n - 1 || keys[i + 1] != k) cend[k] = (int)(i + 1);
+  flag[i] = (i == 0 || keys[i - 1] != k ||
+             entry_body(cd, k, ids[i], ncells) != entry_body(cd, keys[i - 1], ids[i - 1], ncells)) ? 1 : 0;
+}
+// runs (begin entry, body; run_begin[R] = n) and the per-cell run range
+// [cstart, cend) (cells without entries keep 0, 0)
+__global__ void k_hier_runs(ContactDev cd, const unsigned* keys, const int* ids, long long n, unsigned ncells,
+                            const int* flag, const int* rix, int* run_begin, int* run_body, int* cstart, int* cend) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned k = keys[i];
+  int r = rix[i] + flag[i] - 1;  // run of entry i (rix = exclusive scan of the starts)
+  if (flag[i]) {
+    run_begin[r] = (int)i;
+    run_body[r] = entry_body(cd, k, ids[i], ncells);
+  }
+  if (i == 0 || keys[i - 1] != k) cstart[k] = r;
+  if (i == n - 1 || keys[i + 1] != k) cend[k] = r + 1;
+  if (i == n - 1) run_begin[r + 1] = (int)n;
+}
+
+// visit(e) for the entries of cell runs [r0, r1) whose body is not `own`, in order
+template <class Visit>
+__device__ __forceinline__ void visit_cross_runs(int r0, int r1, int own, const int* run_begin, const int* run_body,
+                                                 Visit visit) {
+  for (int r = r0; r < r1; ++r) {
+    if (run_body[r] == own) continue;
+    for (int e = run_begin[r], e1 = run_begin[r + 1]; e < e1; ++e) visit(e);
+  }
 }
 
 // dist(x_v, T(x)) and the pair's step rate s_v + s_t (cross-body pairs only)
@@ -252,8 +284,8 @@ struct HierOut {
 // deterministic min reduction; COUNT / WRITE: one thread per object.
 template <int MODE>
 __global__ void k_hier_query(HierArgs a, const int* lev, const int* cstart, const int* cend, const int* ids,
-                             const long long* off, long long* cnt, int* cv, int* ct, double* partials,
-                             unsigned* counter, double* out) {
+                             const int* run_begin, const int* run_body, const long long* off, long long* cnt,
+                             int* cv, int* ct, double* partials, unsigned* counter, double* out) {
   HierOut R;
   R.cv = cv; R.ct = ct;
   const int nsv = a.cd.nsv, nobj = nsv + a.cd.nst;
@@ -278,9 +310,8 @@ __global__ void k_hier_query(HierArgs a, const int* lev, const int* cstart, cons
           for (int q = c0[1]; q <= c1[1]; ++q)
             for (int p = c0[0]; p <= c1[0]; ++p) {
               unsigned cell = hier_cell(a, lv, p, q, s);
-              long long f = cstart[cell], l = cend[cell];
               ++R.ncell;
-              visit_cross(f, l, bv, [&](long long e) { return a.cd.tbody[ids[e]]; }, [&](long long e) {
+              visit_cross_runs(cstart[cell], cend[cell], bv, run_begin, run_body, [&](int e) {
                 ++R.nent;
                 int t = ids[e];
                 if (MODE != HIER_MIN) {
@@ -309,9 +340,8 @@ __global__ void k_hier_query(HierArgs a, const int* lev, const int* cstart, cons
           for (int q = c0[1]; q <= c1[1]; ++q)
             for (int p = c0[0]; p <= c1[0]; ++p) {
               unsigned cell = a.g.ncells + hier_cell(a, lv, p, q, s);
-              long long f = cstart[cell], l = cend[cell];
               ++R.ncell;
-              visit_cross(f, l, bt, [&](long long e) { return a.cd.vbody[a.cd.sv[ids[e]]]; }, [&](long long e) {
+              visit_cross_runs(cstart[cell], cend[cell], bt, run_begin, run_body, [&](int e) {
                 ++R.nent;
                 int i = ids[e];
                 int v = a.cd.sv[i];
@@ -447,6 +477,8 @@ inline void hier_prepare(Ctx& C, HierArgs& a, const double* bb) {
     long long cap = std::max<long long>(total + total / 2, 4096);
     h.ka = C.alloc<unsigned>(cap); h.kb = C.alloc<unsigned>(cap);
     h.ia = C.alloc<int>(cap); h.ib = C.alloc<int>(cap);
+    h.flag = C.alloc<int>(cap); h.rix = C.alloc<int>(cap);
+    h.run_begin = C.alloc<int>(cap + 1); h.run_body = C.alloc<int>(cap);
     h.cap = cap;
   }
   h.n = total;
@@ -462,7 +494,16 @@ inline void hier_prepare(Ctx& C, HierArgs& a, const double* bb) {
   JGS2_CUDA(cub::DeviceRadixSort::SortPairs(C.scan_temp, sb, h.ka, h.kb, h.ia, h.ib, (int)total, 0, bits,
                                             C.stream));
   ++C.launches;
-  k_hier_dir<<<grid_for(total), kBlock, 0, C.stream>>>(h.kb, total, h.cstart, h.cend);
+  ContactDev cd = contactdev(C);
+  k_hier_run_flags<<<grid_for(total), kBlock, 0, C.stream>>>(cd, h.kb, h.ib, total, a.g.ncells, h.flag);
+  C.check_launch();
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, h.flag, h.rix, (int)total, C.stream);
+  if (tb > C.scan_temp_bytes) { C.scan_temp = C.alloc<char>(tb); C.scan_temp_bytes = tb; }
+  JGS2_CUDA(cub::DeviceScan::ExclusiveSum(C.scan_temp, tb, h.flag, h.rix, (int)total, C.stream));
+  ++C.launches;
+  k_hier_runs<<<grid_for(total), kBlock, 0, C.stream>>>(cd, h.kb, h.ib, total, a.g.ncells, h.flag, h.rix,
+                                                        h.run_begin, h.run_body, h.cstart, h.cend);
   C.check_launch();
 }
 
@@ -491,7 +532,7 @@ inline double hier_min_ratio(Ctx& C, const double* x, const double* dx, double b
   double m = INFINITY;
   int nobj = C.nsv + C.nst;
   k_hier_query<HIER_MIN><<<red_grid(nobj), kBlock, 0, C.stream>>>(
-      a, C.hier_lev, h.cstart, h.cend, h.ib, nullptr, nullptr, nullptr, nullptr, C.partials + R_CAP * kMaxPartials,
+      a, C.hier_lev, h.cstart, h.cend, h.ib, h.run_begin, h.run_body, nullptr, nullptr, nullptr, nullptr, C.partials + R_CAP * kMaxPartials,
       C.counters + R_CAP, C.res + R_CAP);
   C.check_launch();
   JGS2_CUDA(cudaMemcpyAsync(&m, C.res + R_CAP, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
@@ -553,7 +594,7 @@ inline long long hier_candidates(Ctx& C, const double* x, const double* dx, doub
     C.cand_off = C.alloc<long long>(nobj + 1);
   }
   k_hier_query<HIER_COUNT><<<grid_for(nobj), kBlock, 0, C.stream>>>(
-      a, C.hier_lev, h.cstart, h.cend, h.ib, nullptr, C.cand_cnt, nullptr, nullptr, nullptr, nullptr, nullptr);
+      a, C.hier_lev, h.cstart, h.cend, h.ib, h.run_begin, h.run_body, nullptr, C.cand_cnt, nullptr, nullptr, nullptr, nullptr, nullptr);
   C.check_launch();
   long long total = scan_counts(C, C.cand_cnt, C.cand_off, nobj);
   if (total > budget) return -1;
@@ -565,7 +606,7 @@ inline long long hier_candidates(Ctx& C, const double* x, const double* dx, doub
   }
   if (total == 0) return 0;
   k_hier_query<HIER_WRITE><<<grid_for(nobj), kBlock, 0, C.stream>>>(
-      a, C.hier_lev, h.cstart, h.cend, h.ib, C.cand_off, nullptr, C.cand_v, C.cand_t, nullptr, nullptr, nullptr);
+      a, C.hier_lev, h.cstart, h.cend, h.ib, h.run_begin, h.run_body, C.cand_off, nullptr, C.cand_v, C.cand_t, nullptr, nullptr, nullptr);
   C.check_launch();
   return total;
 }
