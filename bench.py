@@ -353,6 +353,7 @@ def main():
                           "outer_solve(state) from pinned host x, z (x, rotations read back) + "
                           "host velocity update"},
         "gpu_launches": launches,
+        "host_rss_gb": round(__import__("resource").getrusage(__import__("resource").RUSAGE_SELF).ru_maxrss / 2**20, 2),
         "clocks": clk,
         "cpu_baseline": cpu,
     }

@@ -37,18 +37,7 @@ struct TriGridDev {
   const int* tris;                 // triangle ids, ascending within a key
   long long n;
   double inv_cell;
-  const int* over;                 // oversized triangles (cap grid only)
-  const int* n_over;
 };
-
-// Per-triangle query radius: r0 + rscale * max corner |dxr| (dxr may be null).
-__device__ __forceinline__ double tri_radius(const int* st, int t, const double* dxr, double r0,
-                                             double rscale) {
-  if (!dxr) return r0;
-  double s = fmax(fmax(norm3_np(dxr + 3 * st[3 * t]), norm3_np(dxr + 3 * st[3 * t + 1])),
-                  norm3_np(dxr + 3 * st[3 * t + 2]));
-  return r0 + rscale * s;
-}
 
 __device__ __forceinline__ void tri_bounds(const int* st, int t, const double* x, const double* dx,
                                            double gamma, double r, double inv_cell, long long* lo,
@@ -66,34 +55,26 @@ __device__ __forceinline__ void tri_bounds(const int* st, int t, const double* x
   }
 }
 
-constexpr long long kMaxCellsPerTri = 512;
-
 __global__ void k_grid_count(int nst, const int* st, const double* x, const double* dx, double gamma,
-                             double r, const double* dxr, double rscale, double inv_cell,
-                             long long* counts, int* over_count, int* over_list) {
+                             double r, double inv_cell, long long* counts) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t > nst) return;
   if (t == nst) { counts[t] = 0; return; }
   long long lo[3], hi[3];
-  tri_bounds(st, t, x, dx, gamma, tri_radius(st, t, dxr, r, rscale), inv_cell, lo, hi);
+  tri_bounds(st, t, x, dx, gamma, r, inv_cell, lo, hi);
   long long c = (hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1) * (hi[2] - lo[2] + 1);
-  if (over_list && !(c > 0 && c <= kMaxCellsPerTri)) {  // oversized: scanned by every query
-    counts[t] = 0;
-    over_list[atomicAdd(over_count, 1)] = t;
-    return;
-  }
   counts[t] = (c > 0 && c < (1LL << 20)) ? c : (1LL << 40);  // flags garbage (NaN) bounds
 }
 
 __global__ void k_grid_write(int nst, const int* st, const double* x, const double* dx, double gamma,
-                             double r, const double* dxr, double rscale, double inv_cell,
-                             const long long* off, unsigned long long* keys, int* tris) {
+                             double r, double inv_cell, const long long* off, unsigned long long* keys,
+                             int* tris) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nst) return;
   long long lo[3], hi[3];
-  tri_bounds(st, t, x, dx, gamma, tri_radius(st, t, dxr, r, rscale), inv_cell, lo, hi);
+  tri_bounds(st, t, x, dx, gamma, r, inv_cell, lo, hi);
   long long o = off[t];
-  if (off[t + 1] == o) return;  // oversized (listed separately) or empty
+  if (off[t + 1] == o) return;
   for (long long i = lo[0]; i <= hi[0]; ++i)
     for (long long j = lo[1]; j <= hi[1]; ++j)
       for (long long k = lo[2]; k <= hi[2]; ++k) {
@@ -151,34 +132,26 @@ __device__ __forceinline__ unsigned long long point_key(const double* p, double 
 }
 
 inline TriGridDev grid_dev(const TriGrid& g) {
-  return TriGridDev{g.keys_b, g.tris_b, g.n, 1.0 / g.cell, g.over, g.n_over};
+  return TriGridDev{g.keys_b, g.tris_b, g.n, 1.0 / g.cell};
 }
 
 inline void tri_grid_free(TriGrid& g) {
   cudaFree(g.counts); cudaFree(g.off); cudaFree(g.keys_a); cudaFree(g.keys_b);
   cudaFree(g.tris_a); cudaFree(g.tris_b); cudaFree(g.temp);
-  cudaFree(g.over); cudaFree(g.n_over);
   g = TriGrid();
 }
 
-// Build the grid of surface triangles at x + gamma*dx inflated by
-// r + rscale * (max corner |dxr|) per triangle (dxr may be null).
+// Build the grid of surface triangles at x + gamma*dx inflated by r.
 // One host sync (the entry count).
 inline void tri_grid_build(Ctx& C, TriGrid& g, const double* x, const double* dx, double gamma, double r,
-                           double cell, const double* dxr = nullptr, double rscale = 0.0,
-                           bool allow_oversize = false) {
+                           double cell) {
   int nst = C.nst;
   g.cell = cell;
   if (!g.counts) {
     JGS2_CUDA(cudaMalloc(&g.counts, (nst + 1) * sizeof(long long)));
     JGS2_CUDA(cudaMalloc(&g.off, (nst + 1) * sizeof(long long)));
-    JGS2_CUDA(cudaMalloc(&g.over, (nst + 1) * sizeof(int)));
-    JGS2_CUDA(cudaMalloc(&g.n_over, sizeof(int)));
   }
-  JGS2_CUDA(cudaMemsetAsync(g.n_over, 0, sizeof(int), C.stream));
-  k_grid_count<<<grid_for(nst + 1), kBlock, 0, C.stream>>>(nst, C.st, x, dx, gamma, r, dxr, rscale,
-                                                            1.0 / cell, g.counts, g.n_over,
-                                                            allow_oversize ? g.over : nullptr);
+  k_grid_count<<<grid_for(nst + 1), kBlock, 0, C.stream>>>(nst, C.st, x, dx, gamma, r, 1.0 / cell, g.counts);
   C.check_launch();
   size_t tb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tb, g.counts, g.off, nst + 1, C.stream);
@@ -205,8 +178,8 @@ inline void tri_grid_build(Ctx& C, TriGrid& g, const double* x, const double* dx
     g.cap = cap;
   }
   g.n = total;
-  k_grid_write<<<grid_for(nst), kBlock, 0, C.stream>>>(nst, C.st, x, dx, gamma, r, dxr, rscale, 1.0 / cell,
-                                                       g.off, g.keys_a, g.tris_a);
+  k_grid_write<<<grid_for(nst), kBlock, 0, C.stream>>>(nst, C.st, x, dx, gamma, r, 1.0 / cell, g.off, g.keys_a,
+                                                       g.tris_a);
   C.check_launch();
   size_t sb = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, sb, g.keys_a, g.keys_b, g.tris_a, g.tris_b, (int)total, 0, 63,

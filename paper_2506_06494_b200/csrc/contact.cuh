@@ -58,44 +58,6 @@ __global__ void k_pair_count(ContactDev cd, TriGridDev g, int use_grid, const do
   cnt[cd.nplanes * cd.nsv + i] = hits;
 }
 
-// Single-block exclusive scan of n ints (in place into out), total at out[n].
-__global__ void k_scan_excl(const int* in, int* out, int n) {
-  __shared__ int warp_tot[32];
-  __shared__ int carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int base = 0; base < n; base += blockDim.x) {
-    int i = base + threadIdx.x;
-    int v = (i < n) ? in[i] : 0;
-    int s = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int t = __shfl_up_sync(0xffffffffu, s, o);
-      if (lane >= o) s += t;
-    }
-    if (lane == 31) warp_tot[wid] = s;
-    __syncthreads();
-    if (wid == 0) {
-      int w = (lane < (int)(blockDim.x >> 5)) ? warp_tot[lane] : 0;
-      int ws = w;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int t = __shfl_up_sync(0xffffffffu, ws, o);
-        if (lane >= o) ws += t;
-      }
-      warp_tot[lane] = ws - w;
-    }
-    __syncthreads();
-    int excl = carry + warp_tot[wid] + s - v;
-    if (i < n) out[i] = excl;
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) out[n] = carry;
-}
-
 // Pass 2: write pair rows in the reference order (contact.py:224-239).
 __global__ void k_pair_write(ContactDev cd, TriGridDev g, int use_grid, const double* x, const double* dx,
                              double gamma, const int* off, int cap, double* rows, int* flag) {

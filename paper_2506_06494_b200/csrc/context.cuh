@@ -53,8 +53,6 @@ struct TriGrid {
   void* temp = nullptr;
   size_t temp_bytes = 0;
   double cell = 0.0;
-  int* over = nullptr;          // oversized triangles (allow_oversize builds)
-  int* n_over = nullptr;
 };
 
 // Sorted (key, id) entry list of the hierarchical cap grids (hier_grid.cuh).
