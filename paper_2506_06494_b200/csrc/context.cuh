@@ -281,15 +281,21 @@ struct Ctx {
     pending.push_back({cur_phase, {cur_start, stop}});
     cur_phase = -1;
   }
-  void collect_phases() {  // call after a stream sync
+  void collect_phases() {  // call after a stream sync; side-stream intervals may still be running
+    size_t keep = 0;
     for (auto& p : pending) {
+      if (cudaEventQuery(p.second.second) == cudaErrorNotReady) {
+        pending[keep++] = p;
+        continue;
+      }
       float ms = 0.f;
       JGS2_CUDA(cudaEventElapsedTime(&ms, p.second.first, p.second.second));
       phase_ms[p.first] += ms;
       event_pool.push_back(p.second.first);
       event_pool.push_back(p.second.second);
     }
-    pending.clear();
+    pending.resize(keep);
+    cudaGetLastError();  // clear the not-ready status
   }
 
   Factor fac;

@@ -180,12 +180,12 @@ void hessians_join(Ctx& C) {
 // Local systems of the free vertices, or of the vertices in `list` (a
 // Gauss-Seidel colour; the element Hessians are then already in place).
 void local_systems(Ctx& C, double* A_out, double* g_out, double* corr_out, const int* list = nullptr,
-                   int nlist = 0) {
+                   int nlist = 0, bool hess_ready = false) {
   DevModel m = devmodel(C);
   if (list) {
     m.nfree = nlist;
     m.free_list = list;
-  } else {
+  } else if (!hess_ready) {
     hessians_async(C);  // no-op if already in flight
     hessians_join(C);
   }
@@ -324,11 +324,13 @@ __global__ void k_apply_list(const int* list, int n, const double* delta, const 
 // positions, local systems with q0 / corrections, the colour's local search,
 // x += step. Leaves C.x = x0 (sweep start) and C.dx = the summed steps for
 // the global backtracking. Returns sum of grad_sq; acts += activations.
-double gauss_seidel_colours(Ctx& C, int* acts) {
+double gauss_seidel_colours(Ctx& C, int* acts, bool hess_ready) {
   bool guard = C.local_line_search;
   size_t bytes = 3 * (size_t)C.nv * sizeof(double);
-  hessians_async(C);
-  hessians_join(C);
+  if (!hess_ready) {
+    hessians_async(C);
+    hessians_join(C);
+  }
   if (!C.x0) {
     C.x0 = C.alloc<double>(3 * (size_t)C.nv);
     C.gs_gsq = C.alloc<double>(std::max<size_t>(C.color_ptr.size(), 1));
@@ -394,31 +396,38 @@ void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
   if (!rot && !C.rot_valid) throw Error(JGS2_E_ARG, "rotations not set");
   DevModel m = devmodel(C);
   bool guard = C.local_line_search;
+  // Optional (JGS2_HESS_EARLY=1): element Hessians at x (compute-bound FP64,
+  // x only) on the low-priority side stream under the latency-bound pair
+  // detection and vertex pass, joined before the collect. Measured neutral on
+  // B200 (C4 49.2-51.1 vs 50.6 sweeps/s): the Hessian grid saturates the SMs,
+  // so there is little idle time to fill. Overlapping them with the solve
+  // itself is slower (the persistent solve CTAs lose residency: 31.9 vs 26.4
+  // ms/sweep). Default: just before the local systems.
+  static const bool early_env = getenv("JGS2_HESS_EARLY") != nullptr;
+  const bool early = early_env && contact_active(C);
+  if (early) hessians_async(C);
   if (contact_active(C)) {  // pairs at x (local_solver.py:612)
     C.phase_begin(7, 0.0);
     contact_find_pairs(C, C.x, nullptr, 0.0);
     C.phase_end();
     if (contact_infeasible(C)) throw Error(JGS2_E_INFEASIBLE, "barrier distance <= 0 at the sweep start");
   }
-  // (Launching the element Hessians here, on the side stream under the
-  // vertex pass + collect, measured slower on B200: C4 31.9 vs 26.4 ms/sweep.
-  // The persistent solve CTAs then cannot all be resident. They run just
-  // before the local systems instead.)
   vertex_pass(C, rot);
   if (contact_active(C)) {
     C.phase_begin(7, 0.0);
     contact_add_gradients(C);
     C.phase_end();
   }
+  hessians_join(C);  // no-op unless launched above
   collect(C);
   const int npairs_x = C.npairs;  // pairs at the sweep-start x
   const bool gs = C.mode == 1 && C.color_ptr.size() > 1;
   int gs_acts = 0;
   double gs_gradsq = 0.0;
   if (gs) {
-    gs_gradsq = gauss_seidel_colours(C, &gs_acts);
+    gs_gradsq = gauss_seidel_colours(C, &gs_acts, early);
   } else {
-    local_systems(C, nullptr, nullptr, nullptr);
+    local_systems(C, nullptr, nullptr, nullptr, nullptr, 0, early);
     C.phase_begin(6, bytes_final(C));
     if (guard) {
       k_ls_final<<<1, 1, 0, C.stream>>>(C.max_halvings, C.alpha_floor, C.ls_cnt, C.ls_max, C.ls_final);
@@ -557,8 +566,11 @@ jgs2_ctx* jgs2_create(int32_t device) {
   if (n <= 0 || device < 0 || device >= n) return nullptr;
   jgs2_ctx* ctx = new jgs2_ctx();
   ctx->c.device = device;
-  if (cudaSetDevice(device) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking) != cudaSuccess) {
+  // main stream at the highest priority: its latency-bound contact kernels are
+  // scheduled ahead of the side stream's element-Hessian blocks
+  int prio_lo = 0, prio_hi = 0;
+  if (cudaSetDevice(device) != cudaSuccess || cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&ctx->c.stream, cudaStreamNonBlocking, prio_hi) != cudaSuccess) {
     delete ctx;
     return nullptr;
   }
@@ -574,7 +586,7 @@ jgs2_ctx* jgs2_create(int32_t device) {
     C.tres = C.alloc<double>(2 * kTrialBatch);
     C.tflags = C.alloc<int>(kTrialBatch);
     C.hess_count = C.alloc<int>(2);
-    JGS2_CUDA(cudaStreamCreateWithFlags(&C.stream2, cudaStreamNonBlocking));
+    JGS2_CUDA(cudaStreamCreateWithPriority(&C.stream2, cudaStreamNonBlocking, prio_lo));
     JGS2_CUDA(cudaEventCreateWithFlags(&C.ev_fork, cudaEventDisableTiming));
     JGS2_CUDA(cudaEventCreateWithFlags(&C.ev_join, cudaEventDisableTiming));
     cudaFuncSetAttribute(k_element_mplus, cudaFuncAttributeMaxDynamicSharedMemorySize,
