@@ -175,6 +175,13 @@ int32_t jgs2_frame_reset(jgs2_ctx* ctx);
 /* v = (x - x_prev) / h; x_prev = x (assembly.py:346-351). */
 int32_t jgs2_frame_end(jgs2_ctx* ctx);
 int32_t jgs2_get_frame_state(jgs2_ctx* ctx, double* x_prev, double* v);
+/* One timestep from HOST buffers, as harness.run does per frame
+ * (harness.py:187-211: compute_z, initialize_step with the feasibility cap,
+ * outer_solve to tol_dx, step_velocity_update): x_prev, v (nv*3) in, the new
+ * x_prev (= x) and v out (outputs may alias inputs); gravity[3] may be NULL. */
+int32_t jgs2_timestep_host(jgs2_ctx* ctx, const double* x_prev, const double* v, double h,
+                           const double* gravity, double* x_prev_out, double* v_out,
+                           int32_t* iterations, int32_t* converged);
 
 /* ---- per-kernel entry points (parity tests; device state in/out) ------- */
 int32_t jgs2_total_energy(jgs2_ctx* ctx, const double* x, double* energy);

@@ -25,7 +25,7 @@ EXPORTS = (
     "jgs2_sym_free", "jgs2_profile", "jgs2_phase_stats", "jgs2_phase_reset", "jgs2_timer_start",
     "jgs2_timer_stop", "jgs2_pinned_alloc", "jgs2_pinned_free", "jgs2_step_cap",
     "jgs2_set_frame_state", "jgs2_frame_begin", "jgs2_frame_end", "jgs2_get_frame_state",
-    "jgs2_frame_reset",
+    "jgs2_frame_reset", "jgs2_timestep_host",
 )
 PHASES = ("vertex_pass", "collect_rhs", "factor_solve", "cubature_hessians", "local_systems",
           "energy", "update", "contact_pairs", "contact_cap", "contact_trials", "frame_cap")
@@ -141,6 +141,7 @@ def lib():
         "jgs2_frame_end": (i32, [vp]),
         "jgs2_frame_reset": (i32, [vp]),
         "jgs2_get_frame_state": (i32, [vp, P(f64), P(f64)]),
+        "jgs2_timestep_host": (i32, [vp, P(f64), P(f64), f64, P(f64), P(f64), P(f64), P(i32), P(i32)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

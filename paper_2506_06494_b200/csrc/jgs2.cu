@@ -1055,6 +1055,52 @@ int32_t jgs2_frame_end(jgs2_ctx* ctx) {
   });
 }
 
+// One whole timestep from HOST buffers (harness.py:187-211 per frame:
+// compute_z, initialize_step, outer_solve to tol_dx, velocity update): the
+// frame state (x_prev, v) goes h2d, the step runs on the device, and the
+// new (x_prev, v) come back d2h. x_prev_out / v_out may alias the inputs.
+int32_t jgs2_timestep_host(jgs2_ctx* ctx, const double* x_prev, const double* v, double h,
+                           const double* gravity, double* x_prev_out, double* v_out,
+                           int32_t* iterations, int32_t* converged) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (!C.have_model) throw Error(JGS2_E_ARG, "model not set");
+    if (!(h > 0)) throw Error(JGS2_E_ARG, "h must be positive");
+    if (!x_prev || !v) throw Error(JGS2_E_ARG, "x_prev and v are required");
+    size_t n = 3 * (size_t)C.nv;
+    if (!C.xprev) { C.xprev = C.alloc<double>(n); C.vel = C.alloc<double>(n); C.dz = C.alloc<double>(n); }
+    JGS2_CUDA(cudaMemcpyAsync(C.xprev, x_prev, n * sizeof(double), cudaMemcpyHostToDevice, C.stream));
+    JGS2_CUDA(cudaMemcpyAsync(C.vel, v, n * sizeof(double), cudaMemcpyHostToDevice, C.stream));
+    for (int c = 0; c < 3; ++c) C.gravity[c] = gravity ? gravity[c] : 0.0;
+    C.h = h;
+    k_compute_z<<<grid_for(C.nv), kBlock, 0, C.stream>>>(C.nv, C.xprev, C.vel, C.h, C.gravity[0],
+                                                         C.gravity[1], C.gravity[2], C.fixed, C.z, C.dz);
+    C.check_launch();
+    double cap = 1.0;
+    if (contact_active(C)) {
+      C.phase_begin(10, 0.0);
+      cap = contact_step_cap(C, C.xprev, C.dz);
+      C.phase_end();
+    }
+    k_init_x<<<grid_for(3 * (int64_t)C.nv), kBlock, 0, C.stream>>>(C.nv, C.xprev, C.dz, cap, C.x);
+    C.check_launch();
+    int it = 0;
+    bool conv = false;
+    while (it < C.max_outer) {
+      jgs2_sweep_info inf;
+      sweep_core(C, true, &inf);
+      ++it;
+      if (inf.dx_norm < C.tol_dx) { conv = true; break; }
+    }
+    k_velocity<<<grid_for(3 * (int64_t)C.nv), kBlock, 0, C.stream>>>(C.nv, C.h, C.x, C.xprev, C.vel);
+    C.check_launch();
+    if (x_prev_out) JGS2_CUDA(cudaMemcpyAsync(x_prev_out, C.xprev, n * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    if (v_out) JGS2_CUDA(cudaMemcpyAsync(v_out, C.vel, n * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    C.sync();
+    if (iterations) *iterations = it;
+    if (converged) *converged = conv ? 1 : 0;
+  });
+}
+
 int32_t jgs2_get_frame_state(jgs2_ctx* ctx, double* x_prev, double* v) {
   return guarded(ctx, [&](Ctx& C) {
     size_t n = 3 * (size_t)C.nv * sizeof(double);

@@ -373,6 +373,24 @@ class LocalSolver:
             out.append((it, conv))
         return out
 
+    def timestep(self, state, gravity, x_prev_out=None, v_out=None):
+        """One harness timestep from host arrays (harness.py:187-211 per
+        frame: compute_z, capped initialize_step, outer_solve to tol_dx,
+        step_velocity_update) in one ABI call. ``state.x_prev`` / ``state.v``
+        go to the device; the new x_prev and v are written to ``x_prev_out`` /
+        ``v_out`` (default: in place). Returns (iterations, converged)."""
+        xp = L.f64a(state.x_prev)
+        v = L.f64a(state.v)
+        xo = xp if x_prev_out is None else x_prev_out
+        vo = v if v_out is None else v_out
+        g = L.f64a(gravity)
+        it, conv = L.i32(0), L.i32(0)
+        self._call(self._lib.jgs2_timestep_host, L.ptr(xp, L.f64), L.ptr(v, L.f64), float(state.h),
+                   L.ptr(g, L.f64), L.ptr(xo, L.f64), L.ptr(vo, L.f64), C_ref(it), C_ref(conv))
+        if x_prev_out is None:
+            state.x_prev, state.v = xp, v
+        return int(it.value), bool(conv.value)
+
     def run_sweeps(self, budget, episode=None):
         """Continue the device-resident simulation for exactly ``budget``
         sweeps (frames end on convergence; a frame still open when the

@@ -159,6 +159,23 @@ def test_device_frame_driver_matches_reference(golden, name):
         assert rel_err(s.get_x(), g["frame_x_final"][f]) < 1e-9
 
 
+@pytest.mark.parametrize("name", ("beam", "two_body", "cube_drop"))
+def test_host_timestep_matches_reference(golden, name):
+    """One ABI call per frame from host buffers (jgs2_timestep_host): the
+    reference trajectory frame by frame, iteration counts identical, and the
+    velocity update v = (x - x_prev) / h."""
+    from paper_2506_06494_b200.model import SystemState
+    g = golden(name)
+    model, s, h = gpu_solver(g)
+    st = SystemState.initial(model, h)
+    for f in range(g["frame_iterations"].size):
+        xp = st.x_prev.copy()
+        it, conv = s.timestep(st, model.gravity)
+        assert it == int(g["frame_iterations"][f]), (f, it)
+        assert rel_err(st.x_prev, g["frame_x_final"][f]) < 1e-9
+        np.testing.assert_array_equal(st.v, (st.x_prev - xp) / h)
+
+
 @pytest.mark.parametrize("name", ("beam_gs", "cube_drop_gs", "two_body_gs"))
 def test_gauss_seidel_trajectory_matches_reference(golden, name):
     # colour sweeps (local_solver.py:627-649) against the reference's own
