@@ -14,9 +14,12 @@
 //
 // Projection: an LDL^T inertia test returns M unchanged when it is positive
 // definite; otherwise the 9x9 eigendecomposition is computed by Householder
-// tridiagonalisation + implicit QL (EISPACK tred2/tql2 scheme) in
-// per-thread interleaved shared memory, and M+ = Q max(L, 0) Q^T.
+// tridiagonalisation + implicit QL (EISPACK tred2/tql2 scheme) with the
+// eigenvectors in per-thread interleaved shared memory, and
+// M+ = Q max(L, 0) Q^T. Divisions and square roots use the FP64-pipe
+// Newton forms of dmath.cuh (the MUFU.*64H forms saturated the XU pipe).
 #pragma once
+#include "dmath.cuh"
 #include "physics.cuh"
 
 namespace jgs2 {
@@ -39,8 +42,8 @@ __device__ __forceinline__ void reduced_hessian_closed(const double* F, const do
   double C[9];
   cofactor(F, C);
   double ic = frob2(F), J = det3_cof(F, C);
-  double d = k.mu_s * (1.0 - 1.0 / (ic + 1.0));
-  double c1 = 2.0 * k.mu_s / ((ic + 1.0) * (ic + 1.0));
+  double d = k.mu_s * (1.0 - rcp_nr(ic + 1.0));
+  double c1 = div_nr(2.0 * k.mu_s, (ic + 1.0) * (ic + 1.0));
   double s = k.lam_s * (J - k.alpha);
   double a[9], b[9];  // a[3p + r] = (F G)[r][p]
 #pragma unroll
@@ -107,7 +110,7 @@ __device__ __forceinline__ bool is_pos_def9(const double* Mp) {
     for (int k = 0; k < j; ++k) dj -= L[JGS2_PK(j, k)] * L[JGS2_PK(j, k)] * dd[k];
     if (!(dj > 0.0)) return false;
     dd[j] = dj;
-    double inv = 1.0 / dj;
+    double inv = rcp_nr(dj);
 #pragma unroll
     for (int i = j + 1; i < 9; ++i) {
       double v = L[JGS2_PK(i, j)];
@@ -117,135 +120,6 @@ __device__ __forceinline__ bool is_pos_def9(const double* Mp) {
     }
   }
   return true;
-}
-
-// Symmetric 9x9 eigendecomposition (tred2 + tql2) on interleaved shared
-// memory: V(i,j) = V[(9*i+j)*S], d(i) = d[i*S], e(i) = e[i*S].
-template <int S>
-__device__ void sym_eig9_shared(double* V, double* d, double* e) {
-  constexpr int n = 9;
-#define VV(i, j) V[((i) * n + (j)) * S]
-#define DD(i) d[(i) * S]
-#define EE(i) e[(i) * S]
-  for (int j = 0; j < n; ++j) DD(j) = VV(n - 1, j);
-  for (int i = n - 1; i > 0; --i) {
-    double scale = 0.0, h = 0.0;
-    for (int k = 0; k < i; ++k) scale += fabs(DD(k));
-    if (scale == 0.0) {
-      EE(i) = DD(i - 1);
-      for (int j = 0; j < i; ++j) { DD(j) = VV(i - 1, j); VV(i, j) = 0.0; VV(j, i) = 0.0; }
-    } else {
-      const double rs = 1.0 / scale;
-      for (int k = 0; k < i; ++k) { DD(k) *= rs; h += DD(k) * DD(k); }
-      double f = DD(i - 1);
-      double g = sqrt(h);
-      if (f > 0) g = -g;
-      EE(i) = scale * g;
-      h -= f * g;
-      DD(i - 1) = f - g;
-      for (int j = 0; j < i; ++j) EE(j) = 0.0;
-      for (int j = 0; j < i; ++j) {
-        f = DD(j);
-        VV(j, i) = f;
-        g = EE(j) + VV(j, j) * f;
-        for (int k = j + 1; k <= i - 1; ++k) { g += VV(k, j) * DD(k); EE(k) += VV(k, j) * f; }
-        EE(j) = g;
-      }
-      f = 0.0;
-      const double rh = 1.0 / h;
-      for (int j = 0; j < i; ++j) { EE(j) *= rh; f += EE(j) * DD(j); }
-      double hh = f / (h + h);
-      for (int j = 0; j < i; ++j) EE(j) -= hh * DD(j);
-      for (int j = 0; j < i; ++j) {
-        f = DD(j);
-        g = EE(j);
-        for (int k = j; k <= i - 1; ++k) VV(k, j) -= (f * EE(k) + g * DD(k));
-        DD(j) = VV(i - 1, j);
-        VV(i, j) = 0.0;
-      }
-    }
-    DD(i) = h;
-  }
-  for (int i = 0; i < n - 1; ++i) {
-    VV(n - 1, i) = VV(i, i);
-    VV(i, i) = 1.0;
-    double h = DD(i + 1);
-    if (h != 0.0) {
-      const double rh = 1.0 / h;
-      for (int k = 0; k <= i; ++k) DD(k) = VV(k, i + 1) * rh;
-      for (int j = 0; j <= i; ++j) {
-        double g = 0.0;
-        for (int k = 0; k <= i; ++k) g += VV(k, i + 1) * VV(k, j);
-        for (int k = 0; k <= i; ++k) VV(k, j) -= g * DD(k);
-      }
-    }
-    for (int k = 0; k <= i; ++k) VV(k, i + 1) = 0.0;
-  }
-  for (int j = 0; j < n; ++j) { DD(j) = VV(n - 1, j); VV(n - 1, j) = 0.0; }
-  VV(n - 1, n - 1) = 1.0;
-  EE(0) = 0.0;
-  // implicit QL
-  for (int i = 1; i < n; ++i) EE(i - 1) = EE(i);
-  EE(n - 1) = 0.0;
-  double f = 0.0, tst1 = 0.0;
-  const double eps = 2.220446049250313e-16;
-  for (int l = 0; l < n; ++l) {
-    tst1 = fmax(tst1, fabs(DD(l)) + fabs(EE(l)));
-    int m = l;
-    while (m < n) {
-      if (fabs(EE(m)) <= eps * tst1) break;
-      ++m;
-    }
-    if (m == n) m = n - 1;
-    if (m > l) {
-      int iter = 0;
-      do {
-        ++iter;
-        double g = DD(l);
-        double p = (DD(l + 1) - g) / (2.0 * EE(l));
-        double r = sqrt(fma(p, p, 1.0));  // |p| <= ~1/eps: no overflow
-        if (p < 0) r = -r;
-        DD(l) = EE(l) / (p + r);
-        DD(l + 1) = EE(l) * (p + r);
-        double dl1 = DD(l + 1);
-        double h = g - DD(l);
-        for (int i = l + 2; i < n; ++i) DD(i) -= h;
-        f += h;
-        p = DD(m);
-        double c = 1.0, c2 = c, c3 = c;
-        double el1 = EE(l + 1);
-        double s = 0.0, s2 = 0.0;
-        for (int i = m - 1; i >= l; --i) {
-          c3 = c2;
-          c2 = c;
-          s2 = s;
-          g = c * EE(i);
-          h = c * p;
-          double ei = EE(i);
-          r = sqrt(fma(p, p, ei * ei));  // Hessian-scale entries: no overflow in FP64
-          EE(i + 1) = s * r;
-          double ri = 1.0 / r;
-          s = ei * ri;
-          c = p * ri;
-          p = c * DD(i) - s * g;
-          DD(i + 1) = h + s * (c * g + s * DD(i));
-          for (int k = 0; k < n; ++k) {
-            h = VV(k, i + 1);
-            VV(k, i + 1) = s * VV(k, i) + c * h;
-            VV(k, i) = c * VV(k, i) - s * h;
-          }
-        }
-        p = -s * s2 * c3 * el1 * EE(l) / dl1;
-        EE(l) = s * p;
-        DD(l) = c * p;
-      } while (fabs(EE(l)) > eps * tst1 && iter < 60);
-    }
-    DD(l) = DD(l) + f;
-    EE(l) = 0.0;
-  }
-#undef VV
-#undef DD
-#undef EE
 }
 
 // The same tred2 + tql2 (JAMA) with every loop bound a compile-time
@@ -268,11 +142,11 @@ __device__ __forceinline__ void sym_eig9_reg(double* V, double (&d)[9], double (
 #pragma unroll
       for (int j = 0; j < i; ++j) { d[j] = VV(i - 1, j); VV(i, j) = 0.0; VV(j, i) = 0.0; }
     } else {
-      const double rs = 1.0 / scale;
+      const double rs = rcp_nr(scale);
 #pragma unroll
       for (int k = 0; k < i; ++k) { d[k] *= rs; h += d[k] * d[k]; }
       double f = d[i - 1];
-      double g = sqrt(h);
+      double g = sqrt_nr(h);
       if (f > 0) g = -g;
       e[i] = scale * g;
       h -= f * g;
@@ -293,10 +167,10 @@ __device__ __forceinline__ void sym_eig9_reg(double* V, double (&d)[9], double (
         e[j] = g;
       }
       f = 0.0;
-      const double rh = 1.0 / h;
+      const double rh = rcp_nr(h);
 #pragma unroll
       for (int j = 0; j < i; ++j) { e[j] *= rh; f += e[j] * d[j]; }
-      double hh = f / (h + h);
+      double hh = div_nr(f, h + h);
 #pragma unroll
       for (int j = 0; j < i; ++j) e[j] -= hh * d[j];
 #pragma unroll
@@ -317,7 +191,7 @@ __device__ __forceinline__ void sym_eig9_reg(double* V, double (&d)[9], double (
     VV(i, i) = 1.0;
     double h = d[i + 1];
     if (h != 0.0) {
-      const double rh = 1.0 / h;
+      const double rh = rcp_nr(h);
 #pragma unroll
       for (int k = 0; k <= i; ++k) d[k] = VV(k, i + 1) * rh;
 #pragma unroll
@@ -353,10 +227,10 @@ __device__ __forceinline__ void sym_eig9_reg(double* V, double (&d)[9], double (
       do {
         ++iter;
         double g = d[l];
-        double p = (d[l + 1] - g) / (2.0 * e[l]);
-        double r = sqrt(fma(p, p, 1.0));  // |p| <= ~1/eps: no overflow
+        double p = div_nr(d[l + 1] - g, 2.0 * e[l]);
+        double r = sqrt_nr(fma(p, p, 1.0));  // |p| <= ~1/eps: no overflow
         if (p < 0) r = -r;
-        d[l] = e[l] / (p + r);
+        d[l] = div_nr(e[l], p + r);
         d[l + 1] = e[l] * (p + r);
         double dl1 = d[l + 1];
         double h = g - d[l];
@@ -379,9 +253,10 @@ __device__ __forceinline__ void sym_eig9_reg(double* V, double (&d)[9], double (
             g = c * e[i];
             h = c * p;
             double ei = e[i];
-            r = sqrt(fma(p, p, ei * ei));  // Hessian-scale entries: no overflow in FP64
+            double q2 = fma(p, p, ei * ei);  // Hessian-scale entries: no overflow in FP64
+            double ri = rsqrt_nr(q2);
+            r = sqrt_from_rsqrt(q2, ri);
             e[i + 1] = s * r;
-            double ri = 1.0 / r;
             s = ei * ri;
             c = p * ri;
             p = c * d[i] - s * g;
@@ -394,7 +269,7 @@ __device__ __forceinline__ void sym_eig9_reg(double* V, double (&d)[9], double (
             }
           }
         }
-        p = -s * s2 * c3 * el1 * e[l] / dl1;
+        p = div_nr(-s * s2 * c3 * el1 * e[l], dl1);
         e[l] = s * p;
         d[l] = c * p;
       } while (fabs(e[l]) > eps * tst1 && iter < 60);

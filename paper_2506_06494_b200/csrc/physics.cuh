@@ -10,6 +10,7 @@
 #pragma once
 #include <cstdint>
 #include <cmath>
+#include "dmath.cuh"
 
 #define JGS2_HD __host__ __device__ __forceinline__
 
@@ -95,10 +96,13 @@ JGS2_HD void jacobi_eig(double* a, double* V, int max_sweeps = 20) {
         double apq = a[p * N + q];
         if (apq == 0.0) continue;
         double app = a[p * N + p], aqq = a[q * N + q];
-        double theta = (aqq - app) / (2.0 * apq);
-        double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-        if (!isfinite(t)) t = 0.0;  // |theta| overflow: apq negligible
-        double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+        double num = aqq - app, den = 2.0 * apq;
+        double t = 0.0;  // |theta| >= 1e150: apq negligible, t ~ 1/(2 theta) -> 0
+        if (fabs(num) < 1e150 * fabs(den)) {
+          double theta = hd_div(num, den);
+          t = hd_div(theta >= 0.0 ? 1.0 : -1.0, fabs(theta) + hd_sqrt(theta * theta + 1.0));
+        }
+        double c = hd_rsqrt(t * t + 1.0), s = t * c;
         for (int k = 0; k < N; ++k) {
           double akp = a[k * N + p], akq = a[k * N + q];
           a[k * N + p] = c * akp - s * akq;
@@ -162,8 +166,8 @@ JGS2_HD void polar_rotation(const double* A, double* R) {
   if (dot3(c12, v3) < 0.0) { v3[0] = -v3[0]; v3[1] = -v3[1]; v3[2] = -v3[2]; }
   double u1[3], u2[3], u3[3];
   mat3_vec(A, v1, u1);
-  double n1 = sqrt(dot3(u1, u1));
-  u1[0] /= n1; u1[1] /= n1; u1[2] /= n1;
+  double r1 = hd_rsqrt(dot3(u1, u1));
+  u1[0] *= r1; u1[1] *= r1; u1[2] *= r1;
   mat3_vec(A, v2, u2);
   double p = dot3(u1, u2);
   u2[0] -= p * u1[0]; u2[1] -= p * u1[1]; u2[2] -= p * u1[2];
@@ -174,7 +178,8 @@ JGS2_HD void polar_rotation(const double* A, double* R) {
     u2[0] = e[0] - pe * u1[0]; u2[1] = e[1] - pe * u1[1]; u2[2] = e[2] - pe * u1[2];
     n2 = sqrt(dot3(u2, u2));
   }
-  u2[0] /= n2; u2[1] /= n2; u2[2] /= n2;
+  double r2 = hd_rcp(n2);
+  u2[0] *= r2; u2[1] *= r2; u2[2] *= r2;
   cross3(u1, u2, u3);
 #pragma unroll
   for (int r = 0; r < 3; ++r)
