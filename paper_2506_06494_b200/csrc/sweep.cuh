@@ -253,52 +253,81 @@ __device__ double alpha_cap(const LocalArgs& a, int v, const double* d) {
 // Sum_s w_s B_s^T Hcur_s B_s with B_s = blockdiag(R_w) V_s (rows before the
 // R_i conjugation).  rows^T (R_blk H_rest R_blk^T) rows = R_i V^T H_rest V R_i^T
 // because R_w^T R_w = I, so the rest part is the precomputed C_v.
+// One cubature slot: E = sum_k Had(k,:) (x) R_{w_k} rows_k, X += w E^T M+ E.
+__device__ __forceinline__ void sampled_slot(const LocalArgs& a, size_t vs, int u, double w, int4 cv,
+                                             double* X) {
+  const double* rows = a.cub_rows + 36 * vs;
+  const double* M = a.mplus + 45 * (size_t)u;
+  double E[27];
+#pragma unroll
+  for (int i = 0; i < 27; ++i) E[i] = 0.0;
+  int corner[4] = {cv.x, cv.y, cv.z, cv.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    double Bk[9];
+    mat3_mul(a.R + 9 * (size_t)corner[k], rows + 9 * k, Bk);
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+      double hw = kHad(k, p);
+#pragma unroll
+      for (int i = 0; i < 9; ++i) E[9 * p + i] += hw * Bk[i];  // E[(p r), c] = E[9p + 3r + c]
+    }
+  }
+  double T1[27];  // M E
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+      double mij = __ldg(M + tri9(i, j));
+      t0 += mij * E[3 * j]; t1 += mij * E[3 * j + 1]; t2 += mij * E[3 * j + 2];
+    }
+    T1[3 * i] = t0; T1[3 * i + 1] = t1; T1[3 * i + 2] = t2;
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      double k = 0.0;
+#pragma unroll
+      for (int i = 0; i < 9; ++i) k += E[3 * i + c] * T1[3 * i + d];
+      X[3 * c + d] += w * k;
+    }
+}
+
+// The per-slot indices (unique element, corners) of every slot are
+// loaded up front, so the dependent M+/R gathers of all slots start after
+// one memory round trip instead of one per slot (ncu: k_local was
+// long-scoreboard bound). Slot order and arithmetic are unchanged.
+constexpr int kSlotsHoisted = 8;
 __device__ void sampled_inner(const DevModel& m, const LocalArgs& a, int v, double* X) {
 #pragma unroll
   for (int i = 0; i < 9; ++i) X[i] = 0.0;
+  if (m.smax <= kSlotsHoisted) {
+    int us[kSlotsHoisted];
+    int4 cvs[kSlotsHoisted];
+#pragma unroll
+    for (int s = 0; s < kSlotsHoisted; ++s) {
+      us[s] = -1;
+      if (s < m.smax) {
+        size_t vs = (size_t)v * m.smax + s;
+        us[s] = __ldg(a.cub_u + vs);
+        cvs[s] = __ldg(a.cub_verts + vs);
+      }
+    }
+#pragma unroll 1
+    for (int s = 0; s < m.smax; ++s)
+      if (us[s] >= 0) {
+        size_t vs = (size_t)v * m.smax + s;
+        sampled_slot(a, vs, us[s], __ldg(a.cub_w + vs), cvs[s], X);
+      }
+    return;
+  }
   for (int s = 0; s < m.smax; ++s) {
     size_t vs = (size_t)v * m.smax + s;
     int u = a.cub_u[vs];
     if (u < 0) continue;
-    double w = a.cub_w[vs];
-    int4 cv = a.cub_verts[vs];
-    const double* rows = a.cub_rows + 36 * vs;
-    double E[27];
-#pragma unroll
-    for (int i = 0; i < 27; ++i) E[i] = 0.0;
-    int corner[4] = {cv.x, cv.y, cv.z, cv.w};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      double Bk[9];
-      mat3_mul(a.R + 9 * (size_t)corner[k], rows + 9 * k, Bk);
-#pragma unroll
-      for (int p = 0; p < 3; ++p) {
-        double hw = kHad(k, p);
-#pragma unroll
-        for (int i = 0; i < 9; ++i) E[9 * p + i] += hw * Bk[i];  // E[(p r), c] = E[9p + 3r + c]
-      }
-    }
-    const double* M = a.mplus + 45 * (size_t)u;
-    double T1[27];  // M E
-#pragma unroll
-    for (int i = 0; i < 9; ++i) {
-      double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-#pragma unroll
-      for (int j = 0; j < 9; ++j) {
-        double mij = __ldg(M + tri9(i, j));
-        t0 += mij * E[3 * j]; t1 += mij * E[3 * j + 1]; t2 += mij * E[3 * j + 2];
-      }
-      T1[3 * i] = t0; T1[3 * i + 1] = t1; T1[3 * i + 2] = t2;
-    }
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        double k = 0.0;
-#pragma unroll
-        for (int i = 0; i < 9; ++i) k += E[3 * i + c] * T1[3 * i + d];
-        X[3 * c + d] += w * k;
-      }
+    sampled_slot(a, vs, u, a.cub_w[vs], a.cub_verts[vs], X);
   }
 }
 
