@@ -63,16 +63,20 @@ k_energy_batch(DevModel m, const double* __restrict__ x0, const double* __restri
       for (int q = 0; q < 9; ++q) D[q] = __ldg(m.dminv + 9 * (size_t)i + q);
       double4 ep = m.eprops[i];
       SnhConst kc = snh_const(ep.y, ep.z);
+      // F is affine in gamma: F(x + gamma dx) = F(x) + gamma F(dx), one
+      // 9-FMA update per trial instead of forming x + gamma dx and Ds Dm^-1
+      // again (the kernel is FP64-pipe bound: ncu 64% active). gamma = 0
+      // gives F(x) exactly; trial energies move by ~1e-15 relative, far
+      // inside the 1e-12 acceptance slack (local_solver.py:566-571).
+      double F0[9], dF[9];
+      deformation_gradient(xb[0], xb[1], xb[2], xb[3], D, F0);
+      deformation_gradient(db[0], db[1], db[2], db[3], D, dF);
 #pragma unroll
       for (int k = 0; k < kTrialBatch; ++k) {
         if (k >= G.n) break;
-        double xs[4][3];
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) xs[a][c] = __dadd_rn(xb[a][c], __dmul_rn(G.g[k], db[a][c]));
         double F[9];
-        deformation_gradient(xs[0], xs[1], xs[2], xs[3], D, F);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) F[q] = fma(G.g[k], dF[q], F0[q]);
         acc[k] += ep.x * snh_psi(F, kc);
       }
     }
