@@ -126,6 +126,7 @@ struct Ctx {
   double tol_dx = 1e-3, alpha_floor = 1e-6;
   int max_outer = 500, max_halvings = 30;
   bool local_line_search = true, track_energy = true;
+  int last_halvings = 0;  // previous sweep's backtracking halvings (sizes the first trial batch)
   int mode = 0;                // 0 jacobi, 1 gauss_seidel
   // Gauss-Seidel colour groups: free vertices by colour (ascending id)
   std::vector<int> color_ptr;

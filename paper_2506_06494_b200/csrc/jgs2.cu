@@ -478,7 +478,9 @@ void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
     while (accepted < 0 && next <= MH) {
       int n = 0, base = next;
       if (first) gb[n++] = 0.0;  // e_before rides in the first batch
-      int want = first ? 1 : kTrialBatch;
+      // the first batch carries e_before plus one trial, or a full batch when
+      // the previous sweep needed halvings (results do not depend on batching)
+      int want = first ? (C.last_halvings > 0 ? kTrialBatch - 1 : 1) : kTrialBatch;
       for (int q = 0; q < want && next <= MH; ++q) gb[n++] = gam[next++];
       if (next > MH && n < kTrialBatch) gb[n++] = gam[MH + 1];  // floor energy (track_energy)
       trial_energies(C, gb, n, Eb, bad);
@@ -512,6 +514,7 @@ void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
       halvings = MH + 1;
       gamma = gam[MH + 1];
     }
+    C.last_halvings = halvings;
   }
   C.phase_begin(6, C.nv * 96.0);
   k_finalize<<<red_grid(C.nv), kBlock, 0, C.stream>>>(C.nv, C.x, C.dx, gamma, guard ? 1 : 0,
