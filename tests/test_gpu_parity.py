@@ -116,7 +116,7 @@ def test_grid_broadphase_pairs_match_bruteforce():
     m, st, h, pre = _c4_small(10)
     s = LocalSolver(m, SolverConfig(), precompute=pre, h_ref=h)
     rng = np.random.default_rng(3)
-    for k in range(4):
+    for k in range(3):
         x = st.x + (0 if k == 0 else 2e-3 * rng.standard_normal(st.x.shape))
         got = s.find_pairs(x)
         ref = orc.find_pairs(m, x).as_rows()
@@ -126,8 +126,10 @@ def test_grid_broadphase_pairs_match_bruteforce():
 
 
 def test_contact_sweeps_match_oracle():
-    """Three JGS2 sweeps with plane + vertex-triangle contact on 10 bodies:
-    GPU vs CPU oracle (same injected precompute, same Hbar)."""
+    """Two JGS2 sweeps with plane + vertex-triangle contact on 10 bodies:
+    GPU vs CPU oracle (same injected precompute, same Hbar). The oracle's
+    brute-force find_pairs runs once per backtracking trial, so each oracle
+    sweep costs minutes on the GPU box's host."""
     from paper_2506_06494_b200.model import SystemState
     m, st, h, pre = _c4_small(6)
     hbar = orc.rest_hessian(m, h)
@@ -135,7 +137,7 @@ def test_contact_sweeps_match_oracle():
     o = orc.OracleSolver(m, pre, h, orc.OracleConfig(), factor=orc.rest_factor(hbar))
     a = SystemState(x=st.x.copy(), x_prev=st.x_prev.copy(), v=st.v.copy(), z=st.z.copy(), h=h)
     b = SystemState(x=st.x.copy(), x_prev=st.x_prev.copy(), v=st.v.copy(), z=st.z.copy(), h=h)
-    for _ in range(3):
+    for _ in range(2):
         assert pair_key(s.find_pairs(a.x)) == pair_key(orc.find_pairs(m, b.x).as_rows())
         dxa, ia = s.sweep(a, s.rotations(a.x))
         dxb, ib = o.sweep(b, orc.vertex_rotations(m, b.x))
