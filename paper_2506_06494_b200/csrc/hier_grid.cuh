@@ -814,8 +814,8 @@ inline long long hier_candidates(Ctx& C, const double* x, const double* dx, doub
     C.cand_cap = cap;
   }
   if (total == 0) return 0;
-  k_hier_query<HIER_WRITE><<<grid_for(nobj), kBlock, 0, C.stream>>>(
-      a, C.hier_lev, h.cstart, h.cend, h.ib, h.run_begin, h.run_body, C.cand_off, nullptr, C.cand_v, C.cand_t, nullptr, nullptr, nullptr);
+  k_hier_write_grp<<<grid_for((int64_t)nobj * kHierGroup), kBlock, 0, C.stream>>>(
+      a, C.hier_lev, h.cstart, h.cend, h.ib, h.run_begin, h.run_body, C.cand_off, C.cand_v, C.cand_t);
   C.check_launch();
   return total;
 }
