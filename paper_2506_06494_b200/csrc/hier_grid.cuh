@@ -278,103 +278,20 @@ struct HierOut {
   }
 };
 
-// One query per object: a vertex scans the triangle grid at its level (big:
-// all triangles but the big ones, which are the triangle side's), a triangle
-// the vertex grid at its level (big: all vertices). MIN: grid-stride with a
-// deterministic min reduction; COUNT / WRITE: one thread per object.
-template <int MODE>
-__global__ void k_hier_query(HierArgs a, const int* lev, const int* cstart, const int* cend, const int* ids,
-                             const int* run_begin, const int* run_body, const long long* off, long long* cnt,
-                             int* cv, int* ct, double* partials, unsigned* counter, double* out) {
-  HierOut R;
-  R.cv = cv; R.ct = ct;
-  const int nsv = a.cd.nsv, nobj = nsv + a.cd.nst;
-  int o0 = blockIdx.x * blockDim.x + threadIdx.x;
-  int stride = MODE == HIER_MIN ? gridDim.x * blockDim.x : nobj;
-  for (int o = o0; o < nobj; o += stride) {
-    if (MODE == HIER_WRITE) R.o = off[o];
-    int lv = lev[o];
-    if (o < nsv) {  // ---- vertex side
-      int v = a.cd.sv[o];
-      int bv = a.cd.vbody[v];
-      if (lv & kHierBig) {
-        for (int t = 0; t < a.cd.nst; ++t)
-          if (a.cd.tbody[t] != bv && !(lev[nsv + t] & kHierBig)) R.take<MODE>(a, v, t);
-      } else {
-        double lo[3], hi[3], tl[3], th[3];
-        vtx_box(a, v, vtx_rho(a, v), lo, hi);
-        double inv = level_inv(a, lv);
-        int c0[3], c1[3];
-        box_cells(a, lv, lo, hi, c0, c1);
-        for (int s = c0[2]; s <= c1[2]; ++s)
-          for (int q = c0[1]; q <= c1[1]; ++q)
-            for (int p = c0[0]; p <= c1[0]; ++p) {
-              unsigned cell = hier_cell(a, lv, p, q, s);
-              ++R.ncell;
-              visit_cross_runs(cstart[cell], cend[cell], bv, run_begin, run_body, [&](int e) {
-                ++R.nent;
-                int t = ids[e];
-                if (MODE != HIER_MIN) {
-                  tri_box(a, t, tri_rho(a, t), tl, th);
-                  if (!owns_pair(a, lv, lo, tl, inv, p, q, s)) return;
-                }
-                R.take<MODE>(a, v, t);
-              });
-            }
-      }
-    } else {  // ---- triangle side
-      int t = o - nsv;
-      int bt = a.cd.tbody[t];
-      if (lv & kHierBig) {
-        for (int i = 0; i < nsv; ++i) {
-          int v = a.cd.sv[i];
-          if (a.cd.vbody[v] != bt) R.take<MODE>(a, v, t);
-        }
-      } else {
-        double lo[3], hi[3], vl[3], vh[3];
-        tri_box(a, t, tri_rho(a, t), lo, hi);
-        double inv = level_inv(a, lv);
-        int c0[3], c1[3];
-        box_cells(a, lv, lo, hi, c0, c1);
-        for (int s = c0[2]; s <= c1[2]; ++s)
-          for (int q = c0[1]; q <= c1[1]; ++q)
-            for (int p = c0[0]; p <= c1[0]; ++p) {
-              unsigned cell = a.g.ncells + hier_cell(a, lv, p, q, s);
-              ++R.ncell;
-              visit_cross_runs(cstart[cell], cend[cell], bt, run_begin, run_body, [&](int e) {
-                ++R.nent;
-                int i = ids[e];
-                int v = a.cd.sv[i];
-                if (MODE != HIER_MIN) {
-                  if ((lev[i] & ~kHierBig) >= lv) return;  // level tie: the vertex side has it
-                  vtx_box(a, v, vtx_rho(a, v), vl, vh);
-                  if (!owns_pair(a, lv, lo, vl, inv, p, q, s)) return;
-                }
-                R.take<MODE>(a, v, t);
-              });
-            }
-      }
-    }
-    if (MODE == HIER_COUNT) cnt[o] = R.n, R.n = 0;
-  }
-  R.flush(a);
-  if (MODE == HIER_MIN) grid_reduce<OP_MIN>(R.mn, partials, counter, out);
-}
-
 // Grouped form of the MIN and COUNT queries: kHierGroup lanes per object,
 // the object's cells (or, for big objects, the opposing objects) strided
 // over the lanes. Per-object work varies by orders of magnitude (box sizes
 // follow the step rates), and one thread per object left the launch a
 // long tail (ncu: 6-7% achieved occupancy of 25% theoretical, IPC 0.4).
 // MIN is a min and COUNT an integer sum, so both results are identical to
-// the one-thread form; WRITE keeps one thread per object, which fixes the
-// candidate order (offsets come from the identical counts).
+// a sequential per-object scan; WRITE (k_hier_write_grp) keeps that scan's
+// candidate order.
 constexpr int kHierGroup = 8;
 template <int MODE>
 __global__ void k_hier_query_grp(HierArgs a, const int* lev, const int* cstart, const int* cend, const int* ids,
                                  const int* run_begin, const int* run_body, long long* cnt, double* partials,
                                  unsigned* counter, double* out) {
-  static_assert(MODE != HIER_WRITE, "WRITE keeps one thread per object");
+  static_assert(MODE != HIER_WRITE, "WRITE is k_hier_write_grp");
   HierOut R;
   const int nsv = a.cd.nsv, nobj = nsv + a.cd.nst;
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
@@ -460,7 +377,7 @@ __global__ void k_hier_query_grp(HierArgs a, const int* lev, const int* cstart, 
 }
 
 // Item k of object o's query (a cell of its box, or an opposing object for
-// big ones), feeding R.take<MODE> exactly as k_hier_query does.
+// big ones), feeding R.take<MODE>.
 struct HierObj {
   int lv, own, id;   // level, own body, vertex (vertex side) or triangle id
   bool vert, big;
@@ -535,8 +452,8 @@ __device__ __forceinline__ void hier_item(const HierArgs& a, const HierObj& h, i
 // Grouped WRITE: the object's items go to the group in chunks of
 // kHierGroup consecutive items; each lane counts its item's pairs, an
 // in-group scan places them, and the lane writes them. Items, and pairs
-// within an item, land in exactly the one-thread order, so the candidate
-// list is bit-identical to k_hier_query<HIER_WRITE>'s.
+// within an item, land in sequential scan order, so the candidate
+// list is bit-identical to a sequential per-object scan's.
 __global__ void k_hier_write_grp(HierArgs a, const int* lev, const int* cstart, const int* cend, const int* ids,
                                  const int* run_begin, const int* run_body, const long long* off, int* cv,
                                  int* ct) {
