@@ -4,10 +4,16 @@ A *step* is one JGS2 outer iteration (Jacobi sweep in corotated_cubature
 mode incl. rotation refresh, exact reduced collect, sampled corrections,
 local line search and the sweep-level backtracking guard), i.e. one
 ``LocalSolver.outer_solve`` iteration (reference local_solver.py:697-716).
-``value`` = sweeps/s over all ranks with the state resident in HBM;
-``e2e`` = the same through the C-ABI host-buffer call (x, z in from pinned
-host memory, x, dx out, every step). ``--impl reference`` times the CPU
-oracle port of the reference (numpy/SciPy, oracle/) on a bounded sample.
+``value`` = sweeps/s over all ranks with the state resident in HBM, in a
+continuing simulation (frames end at tol_dx); ``sweeps`` carries the
+backtracking statistics of the timed window (halvings histogram, floored
+sweeps, accepted gamma/cap) and ``timestep`` whole frames to tol_dx.
+``e2e`` = sweeps/s through the public API with host buffers: one
+``LocalSolver.timestep`` (jgs2_timestep_host) per frame. The CPU oracle port
+of the reference (numpy/SciPy, oracle/) is timed two ways:
+``cpu_vs_gpu_same_config`` measures both sides on identical small inputs;
+``cpu_baseline`` (and ``--impl reference``) is a per-component
+extrapolation to the full config, labelled as such.
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4|c3|c2|c1]
 """
@@ -79,21 +85,81 @@ class Clocks:
 
 
 # ----------------------------------------------------------------- CPU oracle
-def cpu_sample(config, steps=3, budget_s=25.0):
-    """Time the CPU oracle port (oracle/jgs2_oracle.py) on a bounded sample
-    of the workload and extrapolate to the full scene; returns (seconds per
-    sweep at full size, description).
+# same-config comparisons: each runs on identical inputs on the GPU (device
+# timer) and in the CPU oracle port (oracle/, numpy/SciPy, wall clock)
+COMPARE = ("c1", "c3s4", "c4s6")
 
-    * elastic sweep: the same construction scaled down to ~10K tets
-      (injected precompute), ``steps`` sweeps, median s/sweep scaled linearly
-      in element count (84-89 us/tet/sweep is linear in ne, SURVEY App. C3);
-    * contact scenes (the reference's brute-force proximity
-      needs n_sv x n_st x 3 doubles at C4, petabytes, so it is not runnable):
-      one brute-force find_pairs on the 10-body scene at 6 cells/ball, scaled
-      by n_sv * n_st, times the 3 calls a sweep makes at least (pairs at x,
-      one backtracking trial, the tracked energy; local_solver.py:612, 567,
-      712) -- a lower bound on the reference's contact cost.
-    """
+
+def _compare_case(name):
+    """(model, precompute, initial SystemState, h, description) for a
+    same-config comparison. c1 uses the reference's own precompute (bases +
+    cubature written by tetsolve, tests/golden/c1.npz); the others the
+    injected precompute of the benchmark scenes."""
+    from paper_2506_06494_b200 import scenes
+    from paper_2506_06494_b200.model import Model, SystemState
+    from paper_2506_06494_b200.precompute import Precompute
+    if name == "c1":
+        with np.load(ROOT / "tests" / "golden" / "c1.npz") as d:
+            g = {k: d[k] for k in d.files}
+        m = Model.from_arrays(g)
+        h = float(g["scene_h"][0])
+        st = SystemState(x=g["frame_x_init"][0].copy(), x_prev=g["frame_x_prev"][0].copy(),
+                         v=g["frame_v"][0].copy(), z=g["frame_z"][0].copy(), h=h)
+        return m, Precompute.from_arrays(g), st, h, "C1 cantilever 10,080 tets, reference precompute"
+    m, st, h, desc = scenes.build(name)
+    return m, Precompute.injected(m, h, samples=6, seed=0), st, h, desc
+
+
+def cpu_compare(names=COMPARE, sweeps=2, gpu=True):
+    """Measured GPU and CPU-oracle sweeps/s on the same small configs (the
+    sizes the reference algorithm can run on a CPU), each from
+    the same state for the same ``sweeps`` outer iterations (rotations +
+    sweep + tracked energy, local_solver.py:697-716)."""
+    from oracle import jgs2_oracle as orc
+    from paper_2506_06494_b200.model import SystemState
+    out = []
+    for name in names:
+        m, pre, st, h, desc = _compare_case(name)
+        tol = 1e-300  # a fixed number of sweeps
+        rec = {"config": name, "workload": desc, "tets": int(m.num_elements), "sweeps": sweeps}
+        cp = lambda s: SystemState(x=s.x.copy(), x_prev=s.x_prev.copy(), v=s.v.copy(),  # noqa: E731
+                                   z=s.z.copy(), h=s.h)
+        solver = orc.OracleSolver(m, pre, h, orc.OracleConfig(max_outer=sweeps, tol_dx=tol))
+        s1 = cp(st)
+        t0 = time.perf_counter()
+        sc = solver.outer_solve(s1)
+        t_cpu = time.perf_counter() - t0
+        rec["cpu_sweeps_s"] = sc.outer_iterations / t_cpu
+        rec["cpu_halvings"] = [int(a) for a in sc.line_search_activations]
+        if gpu:
+            from paper_2506_06494_b200.local_solver import LocalSolver, SolverConfig
+            g = LocalSolver(m, SolverConfig(max_outer=sweeps, tol_dx=tol), precompute=pre, h_ref=h)
+            for rep in range(2):  # warm-up pass, then the timed pass (same start state)
+                g.set_state(st.x, st.z, h)
+                g.timer_start()
+                for _ in range(sweeps):
+                    g.sweep_resident(True)
+                ms = g.timer_stop()
+            xg = g.get_x()
+            rec["gpu_sweeps_s"] = sweeps / (ms / 1e3)
+            rec["ratio"] = rec["gpu_sweeps_s"] / rec["cpu_sweeps_s"]
+            rec["max_rel_dx_vs_oracle"] = float(np.abs(xg - s1.x).max() / max(np.abs(s1.x).max(), 1e-300))
+            g.close()
+        out.append(rec)
+    return out
+
+
+def cpu_extrapolate(config, budget_s=20.0):
+    """Per-component CPU-port model of one sweep at the full ``config``
+    (labelled an extrapolation: SURVEY 8(d), the reference cannot run C4's
+    brute-force proximity arrays, n_sv x n_st x 3 doubles). Elastic part:
+    measured s/tet/sweep on a bounded slice of the same construction without
+    contact, times the full element count. Proximity part: measured seconds
+    per (surface vertex x surface triangle) test of the reference's
+    brute-force find_pairs on the 6-cells/ball tank, times n_sv*n_st of the
+    full scene, times the find_pairs calls a productive sweep makes (pairs at
+    x, one accepted trial, the tracked energy: local_solver.py:612, 567, 712).
+    Returns (s/sweep, components dict)."""
     from oracle import jgs2_oracle as orc
     from paper_2506_06494_b200 import scenes
     from paper_2506_06494_b200.precompute import Precompute
@@ -101,32 +167,33 @@ def cpu_sample(config, steps=3, budget_s=25.0):
     name = "c1" if config == "c1" else "c3s4"
     m, st, h, _ = scenes.build(name)
     pre = Precompute.injected(m, h, samples=6, seed=0)
-    solver = orc.OracleSolver(m, pre, h, orc.OracleConfig(max_outer=steps))
+    solver = orc.OracleSolver(m, pre, h, orc.OracleConfig(max_outer=1))
     times = []
     t_all = time.perf_counter()
-    for _ in range(steps):
+    while len(times) < 3 and time.perf_counter() - t_all < budget_s:
         t0 = time.perf_counter()
         rot = orc.vertex_rotations(m, st.x)
         solver.sweep(st, rot)
         times.append(time.perf_counter() - t0)
-        if time.perf_counter() - t_all > budget_s:
-            break
     per_tet = statistics.median(times) / m.num_elements
-    per_sweep = per_tet * m_full.num_elements
-    desc = (f"oracle port: {len(times)} sweeps of {name} ({m.num_elements} tets, injected precompute), "
-            f"median s/sweep scaled linearly by element count to {m_full.num_elements} tets")
+    comp = {"elastic_s_per_sweep": per_tet * m_full.num_elements,
+            "elastic_sample": f"{len(times)} oracle sweeps of {name} ({m.num_elements} tets), "
+                              f"median {statistics.median(times):.3f} s"}
+    total = comp["elastic_s_per_sweep"]
     if m_full.barrier is not None and len(m_full.surface_tris):
         mc, stc, _, _ = scenes.build("c4s6")
         t0 = time.perf_counter()
         orc.find_pairs(mc, stc.x)
         t_fp = time.perf_counter() - t0
-        scale = (len(m_full.surface_vertices) * len(m_full.surface_tris)) / (
-            len(mc.surface_vertices) * len(mc.surface_tris))
-        per_sweep += 3 * t_fp * scale
-        desc += (f" + 3 brute-force find_pairs per sweep: one call on c4s6 ({len(mc.surface_vertices)} sv x "
-                 f"{len(mc.surface_tris)} st) took {t_fp:.2f} s, scaled by n_sv*n_st x{scale:.0f} "
-                 f"(extrapolation; the reference cannot run C4's proximity arrays)")
-    return per_sweep, desc
+        per_test = t_fp / (len(mc.surface_vertices) * len(mc.surface_tris))
+        tests = len(m_full.surface_vertices) * len(m_full.surface_tris)
+        comp["proximity_s_per_sweep"] = 3 * per_test * tests
+        comp["proximity_sample"] = (f"brute-force find_pairs on c4s6 ({len(mc.surface_vertices)} sv x "
+                                    f"{len(mc.surface_tris)} st) {t_fp:.3f} s -> {per_test:.3e} s/test; "
+                                    f"{tests:.3e} tests x 3 calls per sweep at full size")
+        total += comp["proximity_s_per_sweep"]
+    comp["extrapolated"] = True
+    return total, comp
 
 
 def traffic(config, kernel, launches, steps):
@@ -156,13 +223,14 @@ def threads():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     # C4 (3.5M tets, ten puffer balls, IPC) is the configuration BASELINE.json's
     # metric is quoted on; C3 (1M-tet twist, no contact) is the elastic-only case
     ap.add_argument("--config", default=os.environ.get("JGS2_BENCH_CONFIG", "c4"))
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--frames", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     from paper_2506_06494_b200 import replicas
@@ -176,7 +244,8 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        per, sample = cpu_sample(args.config, steps=max(min(args.steps, 3), 1))
+        per, comp = cpu_extrapolate(args.config)
+        measured = cpu_compare(gpu=False) if not args.no_cpu else None
         m_full, _, _, desc = scenes.build(args.config)
         v = 1.0 / per
         cores = threads()
@@ -186,7 +255,10 @@ def main():
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": desc, "parallelism": "1 CPU process"},
                 "cpu_baseline": {"value": v, "unit": "sweeps/s", "cores": cores, "kind": "port",
-                                 "sample": sample},
+                                 "sample": "extrapolated per component (the reference cannot run this "
+                                           "config on a CPU): " + json.dumps(comp),
+                                 "host": host_info()},
+                "measured_small_configs": measured,
                 "e2e": {"value": v, "unit": "sweeps/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
@@ -208,15 +280,15 @@ def main():
     # initialize_step, sweeps to tol_dx, velocity update) continue across
     # the warm-up and timed windows; a step is one sweep.
     solver.set_frame_state(init, m.gravity)
-    episode = getattr(m, "episode_frames", None)
-    solver.run_sweeps(args.warmup, episode)
+    solver.run_sweeps(args.warmup)
     solver.phase_reset()
     solver.profile(True)
     launches0 = solver.kernel_launches
     barrier(dist)
     clocks = Clocks(local)
+    record = []
     solver.timer_start()
-    frames_done = solver.run_sweeps(args.steps, episode)
+    frames_done = solver.run_sweeps(args.steps, record)
     ms = solver.timer_stop()
     barrier(dist)
     clk = clocks.stop()
@@ -225,6 +297,17 @@ def main():
     phases = solver.phase_stats()
     solver.profile(False)
     value = replicas.job_throughput(dist, args.steps, ms / 1e3)
+    hv = np.array([r["halvings"] for r in record])
+    mh = cfg.max_halvings
+    accepted = hv <= mh
+    sweeps_info = {
+        "halvings_hist": {str(k): int(c) for k, c in zip(*np.unique(hv, return_counts=True))},
+        "frac_le5_halvings": float(np.mean(hv <= 5)),
+        "floored": int(np.sum(~accepted)),
+        "mean_gamma_over_cap_accepted": (float(np.mean([r["gamma"] / r["cap"] for r, a in zip(record, accepted)
+                                                        if a and r["cap"] > 0])) if accepted.any() else None),
+        "mean_pairs": float(np.mean([r["n_pairs"] for r in record])),
+    }
 
     # roofline of the dominant HBM-modelled kernel (3x3-block arithmetic +
     # sparse triangular solves; the contact phases are latency/search bound
@@ -235,112 +318,52 @@ def main():
     achieved = d_bytes / (d_ms / 1e3) / 1e9 if d_ms > 0 else 0.0
     total_bytes = sum(p[2] for p in phases.values())
 
-    # one full timestep to the residual tolerance, device-resident
-    solver.timer_start()
-    (ts_iters, ts_conv), = solver.run_frames(1)
-    ts_ms = solver.timer_stop()
+    # whole timesteps to the residual tolerance, device-resident: close the
+    # frame left open by the window (untimed), then time complete frames
+    if getattr(solver, "_frame_open", False):
+        while getattr(solver, "_frame_open", False):
+            solver.run_sweeps(1)
+    ts = []
+    for _ in range(args.frames):
+        solver.timer_start()
+        (it, conv), = solver.run_frames(1)
+        ts.append((it, conv, solver.timer_stop()))
 
     # end-to-end through the public API with HOST buffers: one
     # LocalSolver.timestep call per frame (jgs2_timestep_host: the frame
     # state x_prev, v goes h2d from pinned host memory, compute_z + capped
     # initialize_step + outer_solve to tol_dx + velocity update run on the
-    # device, the new x_prev, v come back d2h), the same episode resets as
-    # the timed window (an episode's first frame reads the initial state)
+    # device, the new x_prev, v come back d2h), continuing the simulation
     import ctypes
     nv = m.num_vertices
-    xp0, o5 = L.pinned_array((nv, 3))
-    vv0, o6 = L.pinned_array((nv, 3))
     xpw, o7 = L.pinned_array((nv, 3))
     vvw, o8 = L.pinned_array((nv, 3))
-    xp0[:], vv0[:] = init.x_prev, init.v
+    xs, vs = solver.get_frame_state()
+    xpw[:], vvw[:] = xs, vs
     e2e_sweeps, e2e_frames, h2d, d2h = 0, 0, 0, 0
     t_e2e = time.perf_counter()
     while e2e_sweeps < args.e2e_steps:
-        first = e2e_frames == 0 or bool(episode and e2e_frames % episode == 0)
-        fs = SystemState(x=None, x_prev=xp0 if first else xpw, v=vv0 if first else vvw, z=None, h=h)
+        fs = SystemState(x=None, x_prev=xpw, v=vvw, z=None, h=h)
         it, _ = solver.timestep(fs, m.gravity, x_prev_out=xpw, v_out=vvw)
         h2d += 2 * xpw.nbytes
         d2h += 2 * xpw.nbytes
         e2e_sweeps += it
         e2e_frames += 1
     e2e = replicas.job_throughput(dist, e2e_sweeps, time.perf_counter() - t_e2e)
-    e2e_h2d, e2e_d2h, e2e_n, e2e_f = h2d, d2h, e2e_sweeps, e2e_frames
 
-    # secondary: the reference harness's own loop around the drop-in
-    # LocalSolver (harness.py run loop): per frame host
-    # compute_z, initialize_step (feasibility cap through the ABI), then
-    # LocalSolver.outer_solve(state) -- x, z uploaded from pinned host memory,
-    # sweeps to tol_dx, x and the rotations read back into pinned memory --
-    # and the host velocity update (in place on preallocated arrays); the same
-    # episode resets as the timed window
-    px, o1 = L.pinned_array((nv, 3))
-    pz, o2 = L.pinned_array((nv, 3))
-    pdz, o3 = L.pinned_array((nv, 3))
-    prot, o4 = L.pinned_array((nv, 9))
-    # from the scene's initial state, like every episode of the timed window
-    xp0, vv0 = np.array(init.x_prev, dtype=np.float64), np.array(init.v, dtype=np.float64)
-    xprev, vel = xp0.copy(), vv0.copy()           # host frame state
-    grav = (h * h) * np.asarray(m.gravity, dtype=np.float64)
-    fixed = np.flatnonzero(np.asarray(m.fixed_mask))
-    inf = L.SweepInfo()
-    lib, ctx = solver._lib, solver._ctx
-    cap_d = L.f64(1.0)
-    e2e_sweeps, e2e_frames, h2d, d2h = 0, 0, 0, 0
-    tdbg = {} if os.environ.get("JGS2_E2E_DEBUG") else None
-
-    def mark(key, t0):
-        if tdbg is not None:
-            tdbg[key] = tdbg.get(key, 0.0) + time.perf_counter() - t0
-            tdbg.setdefault(key + "_list", []).append(round(1e3 * (time.perf_counter() - t0), 2))
-        return time.perf_counter()
-    t_e2e = time.perf_counter()
-    while e2e_sweeps < args.e2e_steps:
-        if episode and e2e_frames and e2e_frames % episode == 0:
-            xprev[:], vel[:] = xp0, vv0
-        t0 = time.perf_counter()
-        np.multiply(vel, h, out=pz)                  # compute_z (assembly.py:165-180), in place
-        pz += xprev
-        pz += grav
-        pz[fixed] = xprev[fixed]
-        np.subtract(pz, xprev, out=pdz)
-        px[:] = xprev
-        t0 = mark("host_z", t0)
-        L.check(lib.jgs2_step_cap(ctx, L.ptr(px, L.f64), L.ptr(pdz, L.f64), ctypes.byref(cap_d)), ctx)
-        t0 = mark("step_cap", t0)
-        pdz *= cap_d.value                           # initialize_step (harness.py:130-134)
-        px += pdz
-        L.check(lib.jgs2_set_state(ctx, L.ptr(px, L.f64), L.ptr(pz, L.f64), h), ctx)
-        h2d += 4 * px.nbytes
-        t0 = mark("set_state", t0)
-        for it in range(cfg.max_outer):              # outer_solve (local_solver.py:688-721)
-            L.check(lib.jgs2_sweep(ctx, 1, ctypes.byref(inf)), ctx)
-            e2e_sweeps += 1
-            if inf.dx_norm < cfg.tol_dx:
-                break
-        t0 = mark("sweeps", t0)
-        L.check(lib.jgs2_get_x(ctx, L.ptr(px, L.f64)), ctx)
-        L.check(lib.jgs2_get_rotations(ctx, L.ptr(prot, L.f64)), ctx)
-        d2h += px.nbytes + prot.nbytes
-        t0 = mark("readback", t0)
-        np.subtract(px, xprev, out=vel)              # step_velocity_update (assembly.py:346-351)
-        vel *= 1.0 / h
-        xprev[:] = px
-        t0 = mark("host_v", t0)
-        e2e_frames += 1
-    e2e_h = replicas.job_throughput(dist, e2e_sweeps, time.perf_counter() - t_e2e)
-    if tdbg is not None:
-        print("e2e breakdown (s):", {k: (round(v, 4) if isinstance(v, float) else v) for k, v in tdbg.items()},
-              file=sys.stderr)
-
-    cpu = None
+    cpu, compare = None, None
     if rank == 0 and not args.no_cpu:
         try:
-            per, sample = cpu_sample(args.config)
+            per, comp = cpu_extrapolate(args.config)
             cpu = {"value": 1.0 / per, "unit": "sweeps/s", "cores": threads(), "kind": "port",
-                   "sample": sample}
+                   "sample": "extrapolated per component: " + json.dumps(comp), "host": host_info()}
         except Exception as exc:  # never fail the GPU line on the CPU sample
             cpu = {"value": None, "unit": "sweeps/s", "cores": threads(), "kind": "port",
                    "sample": f"failed: {exc}"}
+        try:
+            compare = cpu_compare()
+        except Exception as exc:
+            compare = [{"failed": str(exc)}]
     if rank != 0:
         return
     line = {
@@ -350,14 +373,13 @@ def main():
         "data": "synthetic",
         "config": {"workload": desc, "tets": m.num_elements, "vertices": nv,
                    "precompute": "injected (structurally valid; Precompute.injected)",
-                   "cubature_samples": 6, "h": h, "parallelism": f"replicas x{world}",
+                   "cubature_samples": 6, "h": h, "tol_dx": cfg.tol_dx, "parallelism": f"replicas x{world}",
                    "l2": "inputs > L2 (factor %.2f GB)" % (8 * fi.nnz_dof / 1e9)},
-        "episode_frames": episode,
-        "timestep": {"iterations": ts_iters, "converged": ts_conv, "ms": ts_ms,
-                     "frames_in_window": len(frames_done),
-                     "mean_sweeps_per_frame": (float(np.mean(frames_done)) if frames_done else None),
-                     "ms_per_timestep": (ms / args.steps * float(np.mean(frames_done))
-                                         if frames_done else None)},
+        "sweeps": sweeps_info,
+        "timestep": {"frames": [{"sweeps": it, "converged": cv, "ms": round(t, 2)} for it, cv, t in ts],
+                     "ms_per_timestep": float(np.mean([t for _, _, t in ts])) if ts else None,
+                     "mean_sweeps_per_frame": float(np.mean([it for it, _, _ in ts])) if ts else None,
+                     "frames_completed_in_window": frames_done},
         "factor": {"nnz_L": int(fi.nnz_dof), "fronts": int(fi.nfronts), "levels": int(fi.nlevels),
                    "max_front": int(fi.max_front), "ordering": "geometric nested dissection",
                    "factor_s": round(solver.factor_seconds, 2), "precompute_s": round(t_pre, 2)},
@@ -371,25 +393,42 @@ def main():
         "phases_ms_per_step": {p: round(v[0] / args.steps, 4) for p, v in phases.items()},
         "phases_gbs": {p: round(v[2] / (v[0] / 1e3) / 1e9, 1) for p, v in phases.items()
                        if v[0] > 0 and v[2] > 0},
-        "e2e": {"value": e2e, "unit": "sweeps/s", "h2d_bytes_per_step": e2e_h2d / max(e2e_n, 1),
-                "d2h_bytes_per_step": e2e_d2h / max(e2e_n, 1), "sweeps": e2e_n, "frames": e2e_f,
+        "e2e": {"value": e2e, "unit": "sweeps/s", "h2d_bytes_per_step": h2d / max(e2e_sweeps, 1),
+                "d2h_bytes_per_step": d2h / max(e2e_sweeps, 1), "sweeps": e2e_sweeps, "frames": e2e_frames,
                 "timing": "wall clock: one LocalSolver.timestep (jgs2_timestep_host) per frame: "
                           "x_prev, v h2d from pinned host memory, compute_z + capped initialize_step "
                           "+ outer_solve to tol_dx + velocity update on the device, x_prev, v d2h"},
-        "e2e_harness_loop": {"value": e2e_h, "unit": "sweeps/s", "h2d_bytes_per_step": h2d / max(e2e_sweeps, 1),
-                             "d2h_bytes_per_step": d2h / max(e2e_sweeps, 1), "sweeps": e2e_sweeps,
-                             "frames": e2e_frames,
-                             "timing": "wall clock: the reference harness loop around the drop-in: per frame "
-                                       "host numpy compute_z + capped initialize_step + outer_solve(state) from "
-                                       "pinned host x, z (x, rotations read back) + host numpy velocity update"},
         "gpu_launches": launches,
         "host_rss_gb": round(__import__("resource").getrusage(__import__("resource").RUSAGE_SELF).ru_maxrss / 2**20, 2),
         "clocks": clk,
         "cpu_baseline": cpu,
+        "cpu_vs_gpu_same_config": compare,
     }
     print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()
+
+
+def host_info():
+    """CPU model, threads and the numpy/SciPy/BLAS stack."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                info["cpu"] = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    try:
+        import scipy
+        info["numpy"], info["scipy"] = np.__version__, scipy.__version__
+        import threadpoolctl
+        info["blas"] = [{k: i.get(k) for k in ("internal_api", "version", "num_threads")}
+                        for i in threadpoolctl.threadpool_info()]
+    except Exception:
+        pass
+    info["OMP_NUM_THREADS"] = os.environ.get("OMP_NUM_THREADS")
+    return info
 
 
 if __name__ == "__main__":

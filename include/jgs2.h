@@ -99,6 +99,8 @@ typedef struct jgs2_sweep_info {
   int32_t n_pairs;         /* active pairs at the sweep start */
   int32_t n_indefinite;    /* cubature elements whose Hessian needed projection */
   int32_t pad_;
+  double gamma;            /* accepted global step fraction (cap * 2^-halvings) */
+  double cap;              /* feasibility cap of the sweep (1 without contact) */
 } jgs2_sweep_info;
 
 typedef struct jgs2_factor_info {

@@ -76,7 +76,7 @@ class Config(C.Structure):
 class SweepInfo(C.Structure):
     _fields_ = [("line_search_activations", i64), ("max_local_step", f64), ("grad_norm", f64),
                 ("grad_sq", f64), ("dx_norm", f64), ("energy", f64), ("halvings", i32),
-                ("n_pairs", i32), ("n_indefinite", i32), ("pad_", i32)]
+                ("n_pairs", i32), ("n_indefinite", i32), ("pad_", i32), ("gamma", f64), ("cap", f64)]
 
 
 class FactorInfo(C.Structure):

@@ -133,6 +133,8 @@ struct Ctx {
   int* color_verts = nullptr;
   double* x0 = nullptr;        // sweep-start positions (GS)
   double* gs_gsq = nullptr;    // per-colour grad_sq (device)
+  double* cap_x = nullptr;     // jgs2_step_cap scratch (host x, dx in)
+  double* cap_dx = nullptr;
 
   // static device data
   int4* tets = nullptr;

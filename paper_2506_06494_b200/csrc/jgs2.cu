@@ -439,7 +439,7 @@ void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
     C.check_launch();
     C.phase_end();
   }
-  double gamma = 1.0, energy = 0.0;
+  double gamma = 1.0, energy = 0.0, cap_used = 1.0;
   int halvings = 0;
   bool have_energy = false;
   int pairs_at_start = npairs_x;
@@ -465,6 +465,7 @@ void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
       trial_candidates(C, cap, have_bb ? bb : nullptr);
       C.phase_end();
     }
+    cap_used = cap;
     const int MH = C.max_halvings;
     std::vector<double> gam(MH + 2);
     gam[0] = cap;
@@ -550,6 +551,8 @@ void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
     info->energy = energy;
     info->halvings = halvings;
     info->n_pairs = pairs_at_start;
+    info->gamma = gamma;
+    info->cap = cap_used;
   }
 }
 
@@ -1264,13 +1267,15 @@ int32_t jgs2_step_cap(jgs2_ctx* ctx, const double* x, const double* dx, double* 
   return guarded(ctx, [&](Ctx& C) {
     *cap = 1.0;
     if (!contact_active(C)) return;
+    // own scratch (x, dx), so a device-resident frame in flight (C.x) is untouched
     size_t n = 3 * (size_t)C.nv * sizeof(double);
-    double *dxd = nullptr;
-    JGS2_CUDA(cudaMemcpyAsync(C.x, x, n, cudaMemcpyHostToDevice, C.stream));
-    JGS2_CUDA(cudaMallocAsync(&dxd, n, C.stream));
-    JGS2_CUDA(cudaMemcpyAsync(dxd, dx, n, cudaMemcpyHostToDevice, C.stream));
-    *cap = contact_step_cap(C, C.x, dxd);
-    JGS2_CUDA(cudaFreeAsync(dxd, C.stream));
+    if (!C.cap_x) {
+      C.cap_x = C.alloc<double>(3 * (size_t)C.nv);
+      C.cap_dx = C.alloc<double>(3 * (size_t)C.nv);
+    }
+    JGS2_CUDA(cudaMemcpyAsync(C.cap_x, x, n, cudaMemcpyHostToDevice, C.stream));
+    JGS2_CUDA(cudaMemcpyAsync(C.cap_dx, dx, n, cudaMemcpyHostToDevice, C.stream));
+    *cap = contact_step_cap(C, C.cap_x, C.cap_dx);
     C.sync();
   });
 }

@@ -294,7 +294,8 @@ class LocalSolver:
                 "grad_norm": float(inf.grad_norm), "grad_sq": float(inf.grad_sq),
                 "dx_norm": float(inf.dx_norm), "energy": float(inf.energy),
                 "halvings": int(inf.halvings), "n_pairs": int(inf.n_pairs),
-                "n_indefinite": int(inf.n_indefinite)}
+                "n_indefinite": int(inf.n_indefinite), "gamma": float(inf.gamma),
+                "cap": float(inf.cap)}
 
     # ------------------------------------------------------------ hot path
     def sweep(self, state, rotations=None):
@@ -378,43 +379,49 @@ class LocalSolver:
         frame: compute_z, capped initialize_step, outer_solve to tol_dx,
         step_velocity_update) in one ABI call. ``state.x_prev`` / ``state.v``
         go to the device; the new x_prev and v are written to ``x_prev_out`` /
-        ``v_out`` (default: in place). Returns (iterations, converged)."""
+        ``v_out`` (default: in place, and then ``state.x`` = the new x and
+        ``state.z`` = the frame's z, as compute_z / step_velocity_update leave
+        them, assembly.py:165-180, 346-351). Returns (iterations, converged)."""
         xp = L.f64a(state.x_prev)
         v = L.f64a(state.v)
-        xo = xp if x_prev_out is None else x_prev_out
+        in_place = x_prev_out is None
+        if in_place:  # the frame's z (compute_z) from the inputs, before they are overwritten
+            z = xp + state.h * v + state.h ** 2 * np.asarray(gravity, dtype=np.float64)
+            fm = np.asarray(self.model.fixed_mask)
+            z[fm] = xp[fm]
+        xo = xp if in_place else x_prev_out
         vo = v if v_out is None else v_out
         g = L.f64a(gravity)
         it, conv = L.i32(0), L.i32(0)
         self._call(self._lib.jgs2_timestep_host, L.ptr(xp, L.f64), L.ptr(v, L.f64), float(state.h),
                    L.ptr(g, L.f64), L.ptr(xo, L.f64), L.ptr(vo, L.f64), C_ref(it), C_ref(conv))
-        if x_prev_out is None:
+        if in_place:
             state.x_prev, state.v = xp, v
+            state.x, state.z = xp.copy(), z
         return int(it.value), bool(conv.value)
 
-    def run_sweeps(self, budget, episode=None):
+    def run_sweeps(self, budget, record=None):
         """Continue the device-resident simulation for exactly ``budget``
-        sweeps (frames end on convergence; a frame still open when the
-        budget runs out is resumed by the next call). With ``episode`` = E,
-        the frame state is restored (device copy) after every E frames.
-        Returns the list of iteration counts of the frames completed."""
+        sweeps (frames end on convergence or max_outer; a frame still open
+        when the budget runs out is resumed by the next call). Per-sweep info
+        dicts are appended to ``record`` when given. Returns the list of
+        iteration counts of the frames completed."""
         done = []
         left = budget
         cap = L.f64(1.0)
         while left > 0:
             if not getattr(self, "_frame_open", False):
-                if episode and getattr(self, "_episode_frames", 0) >= episode:
-                    self._call(self._lib.jgs2_frame_reset)
-                    self._episode_frames = 0
                 self._call(self._lib.jgs2_frame_begin, C_ref(cap))
                 self._frame_open, self._frame_iters = True, 0
             info = self.sweep_resident(refresh_rotations=True)
+            if record is not None:
+                record.append(info)
             left -= 1
             self._frame_iters += 1
             if info["dx_norm"] < self.config.tol_dx or self._frame_iters >= self.config.max_outer:
                 self._call(self._lib.jgs2_frame_end)
                 done.append(self._frame_iters)
                 self._frame_open = False
-                self._episode_frames = getattr(self, "_episode_frames", 0) + 1
         return done
 
     def get_frame_state(self):
