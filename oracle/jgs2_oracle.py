@@ -247,11 +247,35 @@ def closest_points(p, tri):
     return np.linalg.norm(p[:, None, :] - q, axis=2), bary
 
 
+# Exact spatial pruning of the vertex-triangle candidates (fixture
+# generation at scale, tests/golden/make_scale_goldens.py): the narrowphase
+# and the row-major order are the brute-force ones; only (vertex, triangle)
+# combinations that cannot be within dhat are skipped. Off by default.
+PRUNE = False
+
+
+def _pruned_candidates(xs, tris_x, dhat):
+    """Superset of the (vertex row, triangle row) pairs with distance < dhat:
+    |p - centroid| < dhat + circumradius bound, row-major order."""
+    from scipy.spatial import cKDTree
+    cen = tris_x.mean(axis=1)
+    rad = np.linalg.norm(tris_x - cen[:, None], axis=2).max(axis=1)
+    tree = cKDTree(xs)
+    lists = tree.query_ball_point(cen, dhat * (1.0 + 1e-9) + rad * (1.0 + 1e-12) + 1e-300)
+    ti = np.repeat(np.arange(len(cen)), [len(l) for l in lists])
+    vi = np.fromiter((v for l in lists for v in l), dtype=np.int64, count=ti.size)
+    order = np.lexsort((ti, vi))
+    return vi[order], ti[order]
+
+
 def find_pairs(model, x):
     """Brute-force active set (assembly.py:122-128 -> contact.py:216-240).
 
     Plane pairs first (plane order, ascending surface vertex), then
     cross-body vertex-triangle pairs in row-major (vertex, triangle) order.
+    With PRUNE the same narrowphase runs per vertex on its candidate
+    triangles only (identical output, checked against brute force in
+    tests/test_oracle_golden.py).
     """
     empty = Pairs(*(np.zeros(0, dtype=np.int64) for _ in range(2)),
                   np.zeros((0, 3), dtype=np.int64), np.zeros(0, dtype=np.int64),
@@ -271,7 +295,24 @@ def find_pairs(model, x):
             rows["d"].append(float(dist[k]))
             rows["bary"].append((0.0, 0.0, 0.0))
     st = np.asarray(model.surface_tris)
-    if len(st) and len(sv):
+    if len(st) and len(sv) and PRUNE:
+        vb, tb = np.asarray(model.vertex_body), np.asarray(model.surface_tri_body)
+        vi, ti = _pruned_candidates(x[sv], x[st], dhat)
+        keep = vb[sv[vi]] != tb[ti]
+        vi, ti = vi[keep], ti[keep]
+        starts = np.flatnonzero(np.r_[True, vi[1:] != vi[:-1]]) if vi.size else np.zeros(0, np.int64)
+        ends = np.r_[starts[1:], vi.size]
+        for a, b in zip(starts, ends):
+            v, tt = vi[a], ti[a:b]
+            dist, bary = closest_points(x[sv[v:v + 1]], x[st[tt]])
+            for j in np.flatnonzero(dist[0] < dhat):
+                rows["kind"].append(TRIANGLE)
+                rows["vertex"].append(int(sv[v]))
+                rows["tri"].append(tuple(int(w) for w in st[tt[j]]))
+                rows["plane"].append(-1)
+                rows["d"].append(float(dist[0, j]))
+                rows["bary"].append(tuple(bary[0, j]))
+    elif len(st) and len(sv):
         dist, bary = closest_points(x[sv], x[st])
         cross = (np.asarray(model.vertex_body)[sv][:, None]
                  != np.asarray(model.surface_tri_body)[None, :])

@@ -171,11 +171,23 @@ ERRORS = {-1: ValueError, -2: RuntimeError, -3: RuntimeError, -4: KeyError, -5: 
           -6: RuntimeError}
 
 
-class FeasibilityError(Exception):
+def _reference_base(module, name):
+    """The reference's own exception class when ``tetsolve`` is importable
+    (energy.py:14, subspace.py:29), so a caller's ``except
+    energy.FeasibilityError`` also catches the GPU path's error; else
+    Exception."""
+    try:
+        import importlib
+        return getattr(importlib.import_module(f"tetsolve.{module}"), name)
+    except Exception:
+        return Exception
+
+
+class FeasibilityError(_reference_base("energy", "FeasibilityError")):
     """A barrier distance reached <= 0 (reference energy.FeasibilityError)."""
 
 
-class PrecomputeError(Exception):
+class PrecomputeError(_reference_base("subspace", "PrecomputeError")):
     """Rest Hessian factorization failed (reference subspace.PrecomputeError)."""
 
 

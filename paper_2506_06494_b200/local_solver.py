@@ -67,13 +67,66 @@ class IterationStats:
     converged: bool = False
 
 
-def hbar_from_superlu(lu):
-    """Rebuild the factored matrix from a SciPy SuperLU: Pr A Pc = L U
-    (the object ``subspace.rest_factorization`` returns, subspace.py:126-130)."""
-    n = lu.shape[0]
-    pr = sp.csc_matrix((np.ones(n), (lu.perm_r, np.arange(n))), shape=(n, n))
-    pc = sp.csc_matrix((np.ones(n), (np.arange(n), lu.perm_c)), shape=(n, n))
-    return (pr.T @ (lu.L @ lu.U) @ pc.T).tocsr()
+def vertex_adjacency(model):
+    """Vertex graph of the mesh (vertices sharing a tet, self loops included):
+    the block pattern of the rest Hessian (assembly.py:194-259)."""
+    tets = np.asarray(model.tets, dtype=np.int64)
+    nv = int(model.num_vertices)
+    r = np.repeat(tets, 4, axis=1).ravel()
+    c = np.tile(tets, (1, 4)).ravel()
+    a = sp.csr_matrix((np.ones(r.size, dtype=np.int8), (r, c)), shape=(nv, nv))
+    a = (a + sp.identity(nv, dtype=np.int8, format="csr")).tocsr()
+    a.sum_duplicates()
+    a.data[:] = 1
+    return a
+
+
+def hbar_from_factor(factor, model):
+    """Recover the matrix a factorization object was built from, on the mesh
+    pattern only, from its ``.solve``-free triangular factors.
+
+    The reference passes ``subspace.rest_factorization(hbar)`` -- a SciPy
+    SuperLU with Pr A Pc = L U (subspace.py:126-130) -- as ``factor``
+    (harness.py:120-127). Forming L U densifies every fill position, so
+    instead A is probed: a distance-2 colouring of the vertex graph groups
+    columns that share no row, and A @ (sum of a colour's unit vectors) for
+    each colour and DOF component is one product with U then L. Each probe
+    entry at a row adjacent to the colour's column is exactly one A entry.
+    Cost: 3 x colours products with L and U (no fill-sized temporaries).
+    Returns a CSR matrix on the vertex-block pattern."""
+    n = factor.shape[0]
+    adj = vertex_adjacency(model)
+    nv = adj.shape[0]
+    if n != 3 * nv:
+        raise ValueError(f"factor order {n} does not match 3 x {nv} vertices")
+    # distance-2 greedy colouring (ascending vertex id)
+    a2 = (adj @ adj).tocsr()
+    colour = np.full(nv, -1, dtype=np.int64)
+    for v in range(nv):
+        used = colour[a2.indices[a2.indptr[v]:a2.indptr[v + 1]]]
+        taken = np.zeros(used.max(initial=-1) + 2, dtype=bool)
+        taken[used[used >= 0]] = True
+        colour[v] = int(np.flatnonzero(~taken)[0])
+    ncol = int(colour.max()) + 1
+    # probe block: column (3 c + d) = sum over vertices w of colour c of e_{3w+d}
+    cols = (3 * colour[:, None] + np.arange(3)).ravel()
+    rows = np.arange(3 * nv)
+    probe = sp.csc_matrix((np.ones(3 * nv), (rows, cols)), shape=(3 * nv, 3 * ncol))
+    # SciPy's convention Pr A Pc = L U with Pr e_i = e_perm_r[i] and
+    # Pc e_perm_c[i] = e_i, so A x = Pr^T L U Pc^T x, (Pc^T x)[perm_c] = x
+    # and (Pr^T w) = w[perm_r]
+    dense = probe.toarray()
+    z = np.empty_like(dense)
+    z[np.asarray(factor.perm_c)] = dense
+    w = factor.L @ (factor.U @ z)
+    out = w[np.asarray(factor.perm_r)]
+    # scatter back to the block pattern: entry (3v + r, 3w + d) = out[3v + r, 3 colour(w) + d]
+    bp = sp.bsr_matrix((np.ones((adj.nnz, 3, 3)), adj.indices, adj.indptr), shape=(3 * nv, 3 * nv))
+    coo = bp.tocoo()
+    vals = out[coo.row, 3 * colour[coo.col // 3] + coo.col % 3]
+    a = sp.csr_matrix((vals, (coo.row, coo.col)), shape=(3 * nv, 3 * nv))
+    a.eliminate_zeros()
+    return a
 
 
 def matrix_blocks(hbar):
@@ -107,7 +160,7 @@ class LocalSolver:
                 raise ValueError("corotated_cubature needs precomputed bases")
             precompute = Precompute.from_reference(bases, cubature_sets or {})
         if hbar is None and factor is not None and hasattr(factor, "perm_r"):
-            hbar = hbar_from_superlu(factor)
+            hbar = hbar_from_factor(factor, model)
         if hbar is None and h_ref is None:
             if isinstance(factor, (int, float)):
                 h_ref = float(factor)

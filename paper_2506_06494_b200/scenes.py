@@ -165,8 +165,8 @@ def build(name):
         m = cantilever(divisions=(160, 40, 26), extents=(8.0, 2.0, 1.3), young=2e7)
         return m, predictor_state(m, twist_state(m)), H, \
             "C3 stiff beam twist box_grid(160,40,26) 998,400 tets, E=2e7, no contact"
-    if name == "c2":
-        m = puffer_balls(1, cells=45, youngs=(2e7,))
+    if name == "c2" or name.startswith("c2s"):  # c2s<cells>: fewer cells per ball
+        m = puffer_balls(1, cells=45 if name == "c2" else int(name[3:]), youngs=(2e7,))
         m.tol_dx = CONTACT_TOL
         return m, predictor_state(m, SystemState.initial(m, H)), H, \
             f"C2 puffer ball {m.num_elements:,} tets on a ground plane, E=2e7, IPC barrier"

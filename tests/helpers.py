@@ -72,3 +72,31 @@ def replay(g, sweep_fn, pairs_fn, max_frames=None):
         rep["iters_ref"].append(n_ref)
         rep["iters"].append(it)
     return rep
+
+
+def reference_objects(pre):
+    """The reference's precompute objects rebuilt from the flat fixture form:
+    ``{vertex: PerturbationBasis}`` (subspace.py:33-45) and ``{vertex:
+    CubatureSet}`` (cubature.py:22-27) -- the reference's own classes when
+    ``tetsolve`` is importable, else namespaces with the same attributes (the
+    drop-in reads them duck-typed, like the reference's LocalSolver)."""
+    from types import SimpleNamespace
+    try:
+        from tetsolve.subspace import PerturbationBasis
+        from tetsolve.cubature import CubatureSet
+    except Exception:
+        PerturbationBasis = CubatureSet = None
+    bases, sets = {}, {}
+    for k, v in enumerate(np.asarray(pre.vertices)):
+        v = int(v)
+        grp = np.asarray(pre.group[k])
+        grp = grp[grp >= 0]
+        lo, hi = int(pre.vrows_ptr[k]), int(pre.vrows_ptr[k + 1])
+        vrows = {int(w): np.asarray(pre.vrows[j]) for j, w in zip(range(lo, hi), pre.vrows_keys[lo:hi])}
+        kw = dict(vertex=v, gbar=np.asarray(pre.gbar[k]), vrows=vrows, reduced_mass=np.zeros((3, 3)),
+                  group=grp, gbar_rows=np.asarray(pre.gbar_rows[k][:, :3 * grp.size]))
+        bases[v] = PerturbationBasis(**kw) if PerturbationBasis else SimpleNamespace(**kw)
+        c0, c1 = int(pre.cub_ptr[k]), int(pre.cub_ptr[k + 1])
+        ckw = dict(elements=np.asarray(pre.cub_elems[c0:c1]), weights=np.asarray(pre.cub_weights[c0:c1]))
+        sets[v] = CubatureSet(**ckw) if CubatureSet else SimpleNamespace(**ckw)
+    return bases, sets

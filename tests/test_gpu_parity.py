@@ -103,10 +103,12 @@ def test_bit_identical_reruns(golden):
 
 
 # ------------------------------------------------ multi-body contact at scale
-def _c4_small(cells):
+def _c4_small(cells, touching=True):
+    # the tank packed so neighbouring balls touch (c4t): cross-body
+    # vertex-triangle pairs active from the first sweep
     from paper_2506_06494_b200 import scenes
     from paper_2506_06494_b200.precompute import Precompute
-    m, st, h, _ = scenes.build(f"c4s{cells}")
+    m, st, h, _ = scenes.build(f"c4{'t' if touching else 's'}{cells}")
     return m, st, h, Precompute.injected(m, h)
 
 
@@ -200,7 +202,7 @@ def test_gauss_seidel_contact_sweeps_match_oracle():
     # against the oracle's GS on the same inputs
     from paper_2506_06494_b200 import scenes
     from paper_2506_06494_b200.precompute import Precompute
-    m, st, h, _ = scenes.build("c4s6")
+    m, st, h, _ = scenes.build("c4t6")
     pre = Precompute.injected(m, h, samples=6, seed=0)
     cfg = SolverConfig(tol_dx=m.tol_dx, mode="gauss_seidel")
     s = LocalSolver(m, cfg, precompute=pre, hbar=orc.rest_hessian(m, h))
@@ -236,3 +238,27 @@ def test_run_frames_from_reference_cache_matches_reference(golden, tmp_path):
     rows = formats.read_metrics(tmp_path / "metrics.csv")
     assert len(rows) == int(g["frame_iterations"].sum())
     assert (tmp_path / f"frame_{nf:04d}.obj").exists() and (tmp_path / f"body0_frame_{nf:04d}.node").exists()
+
+
+@pytest.mark.parametrize("name", ("beam", "c1", "two_body"))
+def test_drop_in_reference_objects_match_reference(golden, name):
+    """The reference's own call (harness.make_solver, harness.py:120-127):
+    LocalSolver(model, config, bases={v: PerturbationBasis},
+    cubature_sets={v: CubatureSet}, factor=<SciPy SuperLU of Hbar>). The
+    matrix is recovered from the factor on the mesh pattern
+    (hbar_from_factor) and re-factored on the device; every golden frame
+    from its frame-start state reproduces the reference."""
+    import scipy.sparse.linalg as spla
+    from helpers import reference_objects
+    from paper_2506_06494_b200.model import SystemState
+    g = golden(name)
+    model, pre, h = scene_inputs(g)
+    bases, sets = reference_objects(pre)
+    lu = spla.splu(orc.rest_hessian(model, h).tocsc())
+    s = LocalSolver(model, config_of(g), bases, sets, lu)
+    for f in range(g["frame_iterations"].size):
+        st = SystemState(x=g["frame_x_init"][f].copy(), x_prev=g["frame_x_prev"][f].copy(),
+                         v=g["frame_v"][f].copy(), z=g["frame_z"][f].copy(), h=h)
+        stats = s.outer_solve(st)
+        assert stats.outer_iterations == int(g["frame_iterations"][f])
+        assert rel_err(st.x, g["frame_x_final"][f]) < 1e-9
