@@ -192,6 +192,12 @@ int32_t jgs2_reduced_collect(jgs2_ctx* ctx, const double* rotations, const doubl
                              double* q /* nv*3 */);
 int32_t jgs2_sampled_corrections(jgs2_ctx* ctx, double* corr /* nv*9, free rows */);
 int32_t jgs2_reduced_systems(jgs2_ctx* ctx, double* a /* nv*9 */, double* g /* nv*3 */);
+/* Local steps at the device state (x, z, h, rotations): delta = A^-1 (-g)
+ * per vertex (nv*3; _solve_batch, local_solver.py:580-588), the local
+ * search's final step fraction alpha (nv; _line_search + _alpha_caps,
+ * local_solver.py:450-470, 530-553; 1 for fixed vertices) and the
+ * activation count (vertices not accepted at alpha0). */
+int32_t jgs2_local_step(jgs2_ctx* ctx, double* delta, double* alpha, int64_t* activations);
 /* Active pairs at the device x: rows of 10 doubles
  * (kind, vertex, tri0, tri1, tri2, plane, d, bary0, bary1, bary2). */
 int32_t jgs2_find_pairs(jgs2_ctx* ctx, double* rows, int64_t capacity, int64_t* count);

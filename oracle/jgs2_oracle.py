@@ -457,7 +457,9 @@ def feasibility_cap(model, x, dx):
         if np.any(mv):
             cap = min(cap, 0.9 * float(np.min(d[mv] / rate[mv])))
     st = np.asarray(model.surface_tris)
-    if len(model.bodies) > 1 and len(st):
+    if len(model.bodies) > 1 and len(st) and PRUNE:
+        cap = min(cap, _pruned_pair_cap(model, x, dx, sv, st, cap))
+    elif len(model.bodies) > 1 and len(st):
         dist, _ = closest_points(x[sv], x[st])
         cross = (np.asarray(model.vertex_body)[sv][:, None]
                  != np.asarray(model.surface_tri_body)[None, :])
@@ -468,6 +470,36 @@ def feasibility_cap(model, x, dx):
         if np.any(ok):
             cap = min(cap, 0.9 * float(np.min(dist[ok] / rate[ok])))
     return max(cap, 0.0)
+
+
+def _pruned_pair_cap(model, x, dx, sv, st, ub):
+    """0.9 min dist/rate over cross pairs (assembly.py:280-290), skipping only
+    pairs that provably cannot go below the upper bound ``ub``: dist >=
+    |p - centroid| - circumradius and rate <= |dx_v| + max_t |dx_t|. The
+    surviving pairs use the brute-force arithmetic, so the min is identical."""
+    from scipy.spatial import cKDTree
+    p, tri = x[sv], x[st]
+    sp_v = np.linalg.norm(dx[sv], axis=1)
+    sp_t = np.linalg.norm(dx[st], axis=2).max(axis=1)
+    cen = tri.mean(axis=1)
+    rad = float(np.linalg.norm(tri - cen[:, None], axis=2).max())
+    r = (ub / 0.9) * (sp_v + sp_t.max()) * (1.0 + 1e-9) + rad * (1.0 + 1e-12) + 1e-300
+    lists = cKDTree(cen).query_ball_point(p, r)
+    vb, tb = np.asarray(model.vertex_body)[sv], np.asarray(model.surface_tri_body)
+    best = np.inf
+    for vi, tl in enumerate(lists):
+        if not tl:
+            continue
+        tt = np.asarray(tl, dtype=np.int64)
+        tt = tt[tb[tt] != vb[vi]]
+        if not tt.size:
+            continue
+        dist, _ = closest_points(p[vi:vi + 1], tri[tt])
+        rate = sp_v[vi] + sp_t[tt]
+        ok = rate > 1e-30
+        if np.any(ok):
+            best = min(best, float(np.min(dist[0][ok] / rate[ok])))
+    return 0.9 * best if np.isfinite(best) else np.inf
 
 
 # ============================================================ rest factor

@@ -20,7 +20,7 @@ EXPORTS = (
     "jgs2_set_colors", "jgs2_set_state", "jgs2_set_x", "jgs2_get_x", "jgs2_get_dx", "jgs2_set_rotations",
     "jgs2_get_rotations", "jgs2_rotations", "jgs2_sweep", "jgs2_sweep_host",
     "jgs2_outer_solve", "jgs2_total_energy", "jgs2_assembled_field", "jgs2_reduced_collect",
-    "jgs2_sampled_corrections", "jgs2_reduced_systems", "jgs2_find_pairs",
+    "jgs2_sampled_corrections", "jgs2_reduced_systems", "jgs2_local_step", "jgs2_find_pairs",
     "jgs2_last_kernel_launches", "jgs2_sym_build", "jgs2_sym_sizes", "jgs2_sym_export",
     "jgs2_sym_free", "jgs2_profile", "jgs2_phase_stats", "jgs2_phase_reset", "jgs2_timer_start",
     "jgs2_timer_stop", "jgs2_pinned_alloc", "jgs2_pinned_free", "jgs2_step_cap",
@@ -122,6 +122,7 @@ def lib():
         "jgs2_reduced_collect": (i32, [vp, P(f64), P(f64), P(f64)]),
         "jgs2_sampled_corrections": (i32, [vp, P(f64)]),
         "jgs2_reduced_systems": (i32, [vp, P(f64), P(f64)]),
+        "jgs2_local_step": (i32, [vp, P(f64), P(f64), P(i64)]),
         "jgs2_find_pairs": (i32, [vp, P(f64), i64, P(i64)]),
         "jgs2_last_kernel_launches": (i32, [vp, P(i64)]),
         "jgs2_sym_build": (vp, [i64, P(i64), P(i32), P(f64), i32]),

@@ -299,19 +299,7 @@ __global__ void k_apply_list(const int* list, int n, const double* delta, const 
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int v = list[i];
-  double al = 1.0;
-  if (line_search) {
-    int T = lsf[0], fl = lsf[1];
-    int kv = kacc[v];
-    al = alpha0[v];
-    if (kv <= T) {
-      for (int it = 0; it < kv; ++it) al *= 0.5;
-    } else if (fl) {
-      al = alpha_floor;
-    } else {
-      for (int it = 0; it <= max_halvings; ++it) al *= 0.5;
-    }
-  }
+  double al = line_search ? final_alpha(alpha0[v], kacc[v], lsf, max_halvings, alpha_floor) : 1.0;
   for (int c = 0; c < 3; ++c) {
     double st = al * delta[3 * v + c];
     x[3 * v + c] += st;
@@ -1190,6 +1178,33 @@ int32_t jgs2_sampled_corrections(jgs2_ctx* ctx, double* corr) {
 
 int32_t jgs2_reduced_systems(jgs2_ctx* ctx, double* a, double* g) {
   return guarded(ctx, [&](Ctx& C) { debug_systems(C, a, g, nullptr); });
+}
+
+int32_t jgs2_local_step(jgs2_ctx* ctx, double* delta, double* alpha, int64_t* activations) {
+  return guarded(ctx, [&](Ctx& C) {
+    require_ready(C);
+    if (!C.rot_valid) throw Error(JGS2_E_ARG, "rotations not set");
+    if (contact_active(C)) contact_find_pairs(C, C.x, nullptr, 0.0);
+    vertex_pass(C, false);
+    if (contact_active(C)) contact_add_gradients(C);
+    collect(C);
+    local_systems(C, nullptr, nullptr, nullptr);
+    DevModel m = devmodel(C);
+    k_ls_final<<<1, 1, 0, C.stream>>>(C.max_halvings, C.alpha_floor, C.ls_cnt, C.ls_max, C.ls_final);
+    C.check_launch();
+    double* dal = nullptr;
+    JGS2_CUDA(cudaMallocAsync(&dal, (size_t)C.nv * sizeof(double), C.stream));
+    k_alpha_out<<<grid_for(C.nv), kBlock, 0, C.stream>>>(m, C.alpha0, C.kacc, C.ls_final, C.local_line_search ? 1 : 0,
+                                                         C.max_halvings, C.alpha_floor, dal);
+    C.check_launch();
+    int lsf[3] = {0, 0, 0};
+    if (delta) JGS2_CUDA(cudaMemcpyAsync(delta, C.delta, 3 * (size_t)C.nv * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    if (alpha) JGS2_CUDA(cudaMemcpyAsync(alpha, dal, (size_t)C.nv * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    JGS2_CUDA(cudaMemcpyAsync(lsf, C.ls_final, 3 * sizeof(int), cudaMemcpyDeviceToHost, C.stream));
+    JGS2_CUDA(cudaFreeAsync(dal, C.stream));
+    C.sync();
+    if (activations) *activations = C.local_line_search ? lsf[2] : 0;
+  });
 }
 
 int32_t jgs2_find_pairs(jgs2_ctx* ctx, double* rows, int64_t capacity, int64_t* count) {

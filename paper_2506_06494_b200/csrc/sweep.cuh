@@ -444,6 +444,23 @@ __global__ void k_ls_final(int max_halvings, double alpha_floor, const int* cnt,
   out[2] = cnt[0];
 }
 
+// Final local step fraction of one vertex (local_solver.py:539-553): the
+// vertex accepted at halving kv <= T keeps alpha0 2^-kv; vertices still
+// unaccepted after the last halving T take the floor (or 2^-(max+1)).
+__device__ __forceinline__ double final_alpha(double alpha0, int kv, const int* lsf, int max_halvings,
+                                              double alpha_floor) {
+  int T = lsf[0], fl = lsf[1];
+  double al = alpha0;
+  if (kv <= T) {
+    for (int it = 0; it < kv; ++it) al *= 0.5;
+  } else if (fl) {
+    al = alpha_floor;
+  } else {
+    for (int it = 0; it <= max_halvings; ++it) al *= 0.5;
+  }
+  return al;
+}
+
 // dx = alpha * delta for free vertices (local_solver.py:604, 622-624).
 __global__ void __launch_bounds__(kBlock)
 k_apply_alpha(DevModel m, const double* delta, const double* alpha0, const int* kacc,
@@ -454,21 +471,20 @@ k_apply_alpha(DevModel m, const double* delta, const double* alpha0, const int* 
     dx[3 * v] = dx[3 * v + 1] = dx[3 * v + 2] = 0.0;
     return;
   }
-  double al = 1.0;
-  if (line_search) {
-    int T = lsf[0], fl = lsf[1];
-    int kv = kacc[v];
-    al = alpha0[v];
-    if (kv <= T) {
-      for (int it = 0; it < kv; ++it) al *= 0.5;
-    } else if (fl) {
-      al = alpha_floor;
-    } else {
-      for (int it = 0; it <= max_halvings; ++it) al *= 0.5;
-    }
-  }
+  double al = line_search ? final_alpha(alpha0[v], kacc[v], lsf, max_halvings, alpha_floor) : 1.0;
 #pragma unroll
   for (int c = 0; c < 3; ++c) dx[3 * v + c] = al * delta[3 * v + c];
+}
+
+// Per-vertex step fractions of the local search (parity entry point):
+// alpha[v] for free vertices, 1 elsewhere.
+__global__ void __launch_bounds__(kBlock)
+k_alpha_out(DevModel m, const double* alpha0, const int* kacc, const int* lsf, int line_search,
+            int max_halvings, double alpha_floor, double* alpha) {
+  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= m.nv) return;
+  alpha[v] = (m.fixed[v] || m.pos[v] < 0 || !line_search)
+                 ? 1.0 : final_alpha(alpha0[v], kacc[v], lsf, max_halvings, alpha_floor);
 }
 
 // Incremental potential at x0 + gamma*dx (assembly.py:183-192). Elastic

@@ -63,20 +63,23 @@ k_energy_batch(DevModel m, const double* __restrict__ x0, const double* __restri
       for (int q = 0; q < 9; ++q) D[q] = __ldg(m.dminv + 9 * (size_t)i + q);
       double4 ep = m.eprops[i];
       SnhConst kc = snh_const(ep.y, ep.z);
-      // F is affine in gamma: F(x + gamma dx) = F(x) + gamma F(dx), one
-      // 9-FMA update per trial instead of forming x + gamma dx and Ds Dm^-1
-      // again (the kernel is FP64-pipe bound: ncu 64% active). gamma = 0
-      // gives F(x) exactly; trial energies move by ~1e-15 relative, far
-      // inside the 1e-12 acceptance slack (local_solver.py:566-571).
-      double F0[9], dF[9];
-      deformation_gradient(xb[0], xb[1], xb[2], xb[3], D, F0);
-      deformation_gradient(db[0], db[1], db[2], db[3], D, dF);
-#pragma unroll
+      // Each trial forms the rounded positions x_try = fl(x + fl(gamma dx))
+      // and F = Ds(x_try) Dm^-1, exactly as the reference evaluates
+      // total_energy(x_before + gamma * dx) (local_solver.py:564-567). Near
+      // the halving floor E(x_try) - E(x) is at the 1e-12 acceptance slack
+      // and dominated by that rounding of x_try, so an F affine in gamma
+      // (exact arithmetic) would flip accept/reject decisions there.
+#pragma unroll 1
       for (int k = 0; k < kTrialBatch; ++k) {
         if (k >= G.n) break;
-        double F[9];
+        const double g = G.g[k];
+        double xt[4][3];
 #pragma unroll
-        for (int q = 0; q < 9; ++q) F[q] = fma(G.g[k], dF[q], F0[q]);
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) xt[a][c] = __dadd_rn(xb[a][c], __dmul_rn(g, db[a][c]));
+        double F[9];
+        deformation_gradient(xt[0], xt[1], xt[2], xt[3], D, F);
         acc[k] += ep.x * snh_psi(F, kc);
       }
     }

@@ -523,6 +523,17 @@ class LocalSolver:
         self._call(self._lib.jgs2_sampled_corrections, L.ptr(c, L.f64))
         return c[self.free]
 
+    def local_step(self, x, z, h, rotations):
+        """(delta, alpha, activations) of the free vertices: the batched 3x3
+        solves and the local search (local_solver.py:580-604)."""
+        self.set_state(x, z, h)
+        self.set_rotations(rotations)
+        d = np.zeros((self.nv, 3))
+        al = np.ones(self.nv)
+        acts = L.i64(0)
+        self._call(self._lib.jgs2_local_step, L.ptr(d, L.f64), L.ptr(al, L.f64), C_ref(acts))
+        return d[self.free], al[self.free], int(acts.value)
+
     def find_pairs(self, x):
         """Active pair rows (kind, vertex, tri0..2, plane, d, bary0..2)."""
         self._call(self._lib.jgs2_set_x, L.ptr(L.f64a(x), L.f64))

@@ -102,3 +102,23 @@ def test_gauss_seidel_equals_jacobi_without_contact(golden):
     gs, jac = golden("beam_gs"), golden("beam")
     n = gs["traj_x"].shape[0]
     assert np.array_equal(gs["traj_x"], jac["traj_x"][:n])
+
+
+def test_oracle_pruning_is_exact():
+    """The oracle's spatial pruning (used to generate the scale fixtures)
+    returns the brute-force pair table and feasibility cap bit for bit."""
+    from paper_2506_06494_b200 import scenes
+    m, st, h, _ = scenes.build("c4t6")
+    rng = np.random.default_rng(5)
+    x = st.x + 5e-4 * rng.standard_normal(st.x.shape)
+    dx = 0.05 * rng.standard_normal(st.x.shape)
+    try:
+        orc.PRUNE = False
+        a, ca = orc.find_pairs(m, x).as_rows(), orc.feasibility_cap(m, x, dx)
+        orc.PRUNE = True
+        b, cb = orc.find_pairs(m, x).as_rows(), orc.feasibility_cap(m, x, dx)
+    finally:
+        orc.PRUNE = False
+    assert (a[:, 0] == 1).sum() > 0
+    np.testing.assert_array_equal(a, b)
+    assert ca == cb
