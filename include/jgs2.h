@@ -227,6 +227,35 @@ void jgs2_pinned_free(void* p);
  * for the frame driver's initialize_step (harness.py:130-134) */
 int32_t jgs2_step_cap(jgs2_ctx* ctx, const double* x, const double* dx, double* cap);
 
+/* ---- partitioned solve (multi-GPU) ------------------------
+ * One context per GPU, one process per GPU. Each rank owns a contiguous
+ * range of whole bodies (vertex ids [v_begin, v_end), its elements): it
+ * factors and solves its bodies' blocks of the block-diagonal rest Hessian
+ * (the exact collect, local_solver.py:115-126), and runs the vertex pass,
+ * element Hessians and local systems of its vertices. Per sweep the ranks
+ * all-reduce the local-search counters, dx (its owner's rows, zeros
+ * elsewhere), and per-chunk partial sums of the trial energies and grad_sq;
+ * contact detection, the feasibility cap and the backtracking decisions
+ * run replicated on identical data. Results are bit-identical to one GPU.
+ * Call order: create -> set_model -> set_comm_* -> set_partition ->
+ * factor_* -> set_precompute. Jacobi mode only. */
+/* all-reduce callback for jgs2_set_comm_host: reduce host_buf (count
+ * elements; dtype 0 f64, 1 i32, 2 u64; op 0 sum, 1 max) in place across all
+ * ranks; return 0 on success */
+typedef int32_t (*jgs2_allreduce_fn)(void* host_buf, int64_t count, int32_t dtype, int32_t op, void* user);
+/* ncclGetUniqueId (128 bytes), to be broadcast from rank 0 */
+int32_t jgs2_nccl_unique_id(uint8_t* id128);
+/* NCCL communicator created by the context (ncclCommInitRank) */
+int32_t jgs2_set_comm_nccl(jgs2_ctx* ctx, int32_t world, int32_t rank, const uint8_t* id128);
+/* caller-owned ncclComm_t (not destroyed by the context) */
+int32_t jgs2_set_comm_nccl_handle(jgs2_ctx* ctx, int32_t world, int32_t rank, void* nccl_comm);
+/* host-callback collectives (tests: ranks sharing one GPU over gloo) */
+int32_t jgs2_set_comm_host(jgs2_ctx* ctx, int32_t world, int32_t rank, jgs2_allreduce_fn fn, void* user);
+/* own vertices [v_begin, v_end): must start and end at body boundaries */
+int32_t jgs2_set_partition(jgs2_ctx* ctx, int64_t v_begin, int64_t v_end);
+/* context on a caller-provided CUDA stream (cudaStream_t; NULL = own) */
+jgs2_ctx* jgs2_create_on_stream(int32_t device, void* stream);
+
 /* ---- symbolic analysis (host only; no device needed) ------------------ */
 typedef struct jgs2_sym jgs2_sym;
 jgs2_sym* jgs2_sym_build(int64_t n, const int64_t* adj_ptr, const int32_t* adj,

@@ -25,7 +25,8 @@ EXPORTS = (
     "jgs2_sym_free", "jgs2_profile", "jgs2_phase_stats", "jgs2_phase_reset", "jgs2_timer_start",
     "jgs2_timer_stop", "jgs2_pinned_alloc", "jgs2_pinned_free", "jgs2_step_cap",
     "jgs2_set_frame_state", "jgs2_frame_begin", "jgs2_frame_end", "jgs2_get_frame_state",
-    "jgs2_frame_reset", "jgs2_timestep_host",
+    "jgs2_frame_reset", "jgs2_timestep_host", "jgs2_nccl_unique_id", "jgs2_set_comm_nccl",
+    "jgs2_set_comm_nccl_handle", "jgs2_set_comm_host", "jgs2_set_partition", "jgs2_create_on_stream",
 )
 PHASES = ("vertex_pass", "collect_rhs", "factor_solve", "cubature_hessians", "local_systems",
           "energy", "update", "contact_pairs", "contact_cap", "contact_trials", "frame_cap")
@@ -143,6 +144,12 @@ def lib():
         "jgs2_frame_reset": (i32, [vp]),
         "jgs2_get_frame_state": (i32, [vp, P(f64), P(f64)]),
         "jgs2_timestep_host": (i32, [vp, P(f64), P(f64), f64, P(f64), P(f64), P(f64), P(i32), P(i32)]),
+        "jgs2_nccl_unique_id": (i32, [P(u8)]),
+        "jgs2_set_comm_nccl": (i32, [vp, i32, i32, P(u8)]),
+        "jgs2_set_comm_nccl_handle": (i32, [vp, i32, i32, vp]),
+        "jgs2_set_comm_host": (i32, [vp, i32, i32, vp, vp]),
+        "jgs2_set_partition": (i32, [vp, i64, i64]),
+        "jgs2_create_on_stream": (vp, [i32, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -35,6 +35,21 @@ def cuda_lib_dir():
     return root / "lib64"
 
 
+def nccl_dirs():
+    """(include dir, lib dir) of the NCCL torch loads (pip nvidia-nccl), so the
+    library binds the same libnccl.so.2 as torch.distributed; else the system one."""
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia")
+        for root in (spec.submodule_search_locations or []):
+            d = Path(root) / "nccl"
+            if (d / "include" / "nccl.h").exists() and (d / "lib" / "libnccl.so.2").exists():
+                return d / "include", d / "lib"
+    except Exception:
+        pass
+    return Path("/usr/include"), Path("/usr/lib/x86_64-linux-gnu")
+
+
 def stale():
     if not LIB.exists():
         return True
@@ -49,10 +64,12 @@ def build(force=False, verbose=False):
     LIBDIR.mkdir(exist_ok=True)
     libdir = cuda_lib_dir()
     tmp = LIB.with_suffix(f".so.tmp{os.getpid()}")
+    ninc, nlib = nccl_dirs()
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xptxas", "-O3", "-I", str(PKG.parent / "include"),
+           "-Xptxas", "-O3", "-I", str(PKG.parent / "include"), "-I", str(ninc),
            *[str(CSRC / s) for s in SOURCES], "-o", str(tmp),
-           "-L", str(libdir), f"-Xlinker=-rpath,{libdir}", "-lcusolver", "-lcublas"]
+           "-L", str(libdir), f"-Xlinker=-rpath,{libdir}", "-lcusolver", "-lcublas",
+           "-L", str(nlib), f"-Xlinker=-rpath,{nlib}", "-l:libnccl.so.2"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))

@@ -67,6 +67,18 @@ struct HierList {
   long long ncells_cap = 0;
 };
 
+// Collective layer of a partitioned solve (one rank per GPU):
+// in-place all-reduce of device buffers on the context stream. NCCL in
+// production; a host callback (torch.distributed/gloo) for multi-process
+// tests that share one GPU.
+enum CommType { CT_F64 = 0, CT_I32 = 1, CT_U64 = 2 };
+enum CommOp { CO_SUM = 0, CO_MAX = 1 };
+struct Comm {
+  int rank = 0, world = 1;
+  virtual ~Comm() {}
+  virtual void allreduce(void* buf, size_t count, int type, int op, cudaStream_t s) = 0;
+};
+
 // Device-side factor of the free-vertex rest Hessian (supernodal, ND order).
 struct Factor {
   bool ready = false;
@@ -135,6 +147,23 @@ struct Ctx {
   double* gs_gsq = nullptr;    // per-colour grad_sq (device)
   double* cap_x = nullptr;     // jgs2_step_cap scratch (host x, dx in)
   double* cap_dx = nullptr;
+
+  // partition (jgs2_set_partition): this rank owns vertices [own_v0, own_v1)
+  // and elements [own_e0, own_e1) -- whole bodies, so the rest Hessian is
+  // block diagonal across ranks. Reductions run over fixed chunks aligned to
+  // body boundaries, so the result is the same for every rank count.
+  int own_v0 = 0, own_v1 = 0, own_e0 = 0, own_e1 = 0;
+  bool partitioned = false;
+  Comm* comm = nullptr;
+  std::vector<int> body_v, body_e;  // body boundaries (vertex / element ids), size nbodies+1
+  int2* chunks = nullptr;           // element chunks, then vertex chunks: [begin, end)
+  int nchunk_e = 0, nchunk_v = 0;
+  int chunk_own0 = 0, chunk_own1 = 0;      // owned element chunks [c0, c1)
+  int vchunk_own0 = 0, vchunk_own1 = 0;    // owned vertex chunks (global chunk ids)
+  double* cpart = nullptr;          // (kTrialBatch + 1) * nchunks partial sums
+  std::vector<int> chunk_first_e, chunk_first_v;  // first chunk of each body (+ end)
+  bool own_stream = true;
+  bool owns(int v) const { return v >= own_v0 && v < own_v1; }
 
   // static device data
   int4* tets = nullptr;
@@ -328,6 +357,10 @@ struct Ctx {
     ++launches;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw Error(-2, std::string("kernel launch: ") + cudaGetErrorString(e));
+  }
+  // all-reduce of a device buffer across ranks (no-op on one rank)
+  void allreduce(void* buf, size_t count, int type, int op) {
+    if (comm && comm->world > 1) comm->allreduce(buf, count, type, op, stream);
   }
   ~Ctx();
 };

@@ -356,7 +356,7 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
   // ---- free-vertex graph (vertex adjacency through elements, incl. self)
   std::vector<int> loc(nv, -1), glob;
   for (int v = 0; v < nv; ++v)
-    if (!C.h_fixed[v]) { loc[v] = (int)glob.size(); glob.push_back(v); }
+    if (!C.h_fixed[v] && C.owns(v)) { loc[v] = (int)glob.size(); glob.push_back(v); }  // this rank's bodies
   int n = (int)glob.size();
   F.nfree = n;
   std::vector<std::vector<int>> nb(n);

@@ -14,6 +14,8 @@
 #include "contact.cuh"
 #include "trials.cuh"
 #include "hier_grid.cuh"
+#include "partition.cuh"
+#include "comm.cuh"
 
 using namespace jgs2;
 
@@ -33,7 +35,8 @@ jgs2::Ctx::~Ctx() {
   if (ev_join) cudaEventDestroy(ev_join);
   if (stream2) cudaStreamDestroy(stream2);
   if (fac.graph_exec) cudaGraphExecDestroy(fac.graph_exec);
-  if (stream) cudaStreamDestroy(stream);
+  delete comm;
+  if (stream && own_stream) cudaStreamDestroy(stream);
 }
 
 struct jgs2_ctx {
@@ -67,6 +70,7 @@ DevModel devmodel(const Ctx& C) {
   m.nv = C.nv; m.ne = C.ne; m.smax = C.smax; m.gmax = C.gmax; m.nfree = C.nfree;
   m.tets = C.tets; m.dminv = C.dminv; m.eprops = C.eprops; m.inc_ptr = C.inc_ptr; m.inc = C.inc;
   m.mass = C.mass; m.fixed = C.fixed; m.pos = C.pos; m.free_list = C.free_list;
+  m.v0 = C.own_v0; m.v1 = C.own_v1;
   return m;
 }
 
@@ -124,20 +128,36 @@ void launch_energy(Ctx& C, const double* dx, double gamma, int slot) {
 void vertex_pass(Ctx& C, bool rot) {
   DevModel m = devmodel(C);
   C.phase_begin(0, bytes_vertex(C));
-  if (rot) k_vertex_pass<true><<<grid_for(C.nv), kBlock, 0, C.stream>>>(m, C.x, C.z, C.h, C.R, C.gasm);
-  else k_vertex_pass<false><<<grid_for(C.nv), kBlock, 0, C.stream>>>(m, C.x, C.z, C.h, C.R, C.gasm);
+  int nown = C.own_v1 - C.own_v0;  // this rank's vertices (all of them on one GPU)
+  if (rot) k_vertex_pass<true><<<grid_for(nown), kBlock, 0, C.stream>>>(m, C.x, C.z, C.h, C.R, C.gasm);
+  else k_vertex_pass<false><<<grid_for(nown), kBlock, 0, C.stream>>>(m, C.x, C.z, C.h, C.R, C.gasm);
   C.check_launch();
   C.phase_end();
   if (rot) C.rot_valid = true;
 }
 
+// grad_sq over the free vertices (local_solver.py:602-603) in vertex chunks:
+// this rank's chunks, all-reduced, combined in chunk order into res[R_GRADSQ]
+void gradsq_chunks(Ctx& C) {
+  double* row = C.cpart + (size_t)kTrials * (C.nchunk_e + C.nchunk_v);
+  if (C.partitioned)
+    JGS2_CUDA(cudaMemsetAsync(row, 0, (size_t)(C.nchunk_e + C.nchunk_v) * sizeof(double), C.stream));
+  int n = C.vchunk_own1 - C.vchunk_own0;
+  if (n > 0) {
+    k_chunk_gradsq<<<n, kBlock, 0, C.stream>>>(C.chunks, C.vchunk_own0, C.gasm, C.fixed, row);
+    C.check_launch();
+  }
+  C.allreduce(row + C.nchunk_e, C.nchunk_v, CT_F64, CO_SUM);
+  k_reduce_chunks<<<1, kBlock, 0, C.stream>>>(row + C.nchunk_e, C.nchunk_v, 0, 1, C.res + R_GRADSQ);
+  C.check_launch();
+}
+
 void collect(Ctx& C) {
   DevModel m = devmodel(C);
   C.phase_begin(1, bytes_rhs(C));
-  k_rhs<<<red_grid(C.nfree), kBlock, 0, C.stream>>>(m, C.R, C.gasm, C.b,
-                                                     C.partials + R_GRADSQ * kMaxPartials,
-                                                     C.counters + R_GRADSQ, C.res + R_GRADSQ);
+  k_rhs<<<grid_for(C.nfree), kBlock, 0, C.stream>>>(m, C.R, C.gasm, C.b);
   C.check_launch();
+  gradsq_chunks(C);
   C.phase_end();
   C.phase_begin(2, bytes_solve(C));
   factor_solve(C);
@@ -200,6 +220,10 @@ void local_systems(Ctx& C, double* A_out, double* g_out, double* corr_out, const
   a.vr_ptr = C.vr_ptr; a.vr_keys = C.vr_keys; a.vr_rows = C.vr_rows;
   if (m.nfree > 0) k_local<<<grid_for(m.nfree, 128), 128, 0, C.stream>>>(m, a);
   C.check_launch();
+  // the local search's halving rounds are global (local_solver.py:539-553):
+  // counts of unaccepted vertices and the max alpha0 among them per round
+  C.allreduce(C.ls_cnt, C.max_halvings + 2, CT_I32, CO_SUM);
+  C.allreduce(C.ls_max, C.max_halvings + 2, CT_U64, CO_MAX);
   C.phase_end();
 }
 
@@ -222,11 +246,28 @@ void trial_energies(Ctx& C, const double* gam, int n, double* E, bool* infeasibl
   G.n = n;
   for (int k = 0; k < kTrialBatch; ++k) G.g[k] = k < n ? gam[k] : 0.0;
   int grid = red_grid(std::max(C.ne, C.nv));
-  C.phase_begin(5, n * bytes_energy(C, true) / std::max(n, 1) + (n - 1) * 0.0);
-  k_energy_batch<<<grid, kBlock, 0, C.stream>>>(m, C.x, C.dx, G, C.z, C.h, C.tpart);
-  C.check_launch();
-  k_reduce_batch<<<1, kBlock, 0, C.stream>>>(C.tpart, grid, n, C.tres);
-  C.check_launch();
+  C.phase_begin(5, bytes_energy(C, true));
+  {  // elastic + inertia per chunk (this rank's chunks), all-reduced, chunk order
+    const int nch = C.nchunk_e + C.nchunk_v;
+    TrialGammas TG;
+    TG.n = n;
+    for (int k = 0; k < kTrials; ++k) TG.g[k] = G.g[k];
+    if (C.partitioned) JGS2_CUDA(cudaMemsetAsync(C.cpart, 0, (size_t)n * nch * sizeof(double), C.stream));
+    int ne_own = C.chunk_own1 - C.chunk_own0, nv_own = C.vchunk_own1 - C.vchunk_own0;
+    if (ne_own > 0) {
+      k_energy_chunks<<<ne_own, kBlock, 0, C.stream>>>(m, C.chunks, C.chunk_own0, C.nchunk_e, nch, C.x, C.dx,
+                                                        TG, C.z, C.h, C.cpart);
+      C.check_launch();
+    }
+    if (nv_own > 0) {
+      k_energy_chunks<<<nv_own, kBlock, 0, C.stream>>>(m, C.chunks, C.vchunk_own0, C.nchunk_e, nch, C.x, C.dx,
+                                                        TG, C.z, C.h, C.cpart);
+      C.check_launch();
+    }
+    C.allreduce(C.cpart, (size_t)n * nch, CT_F64, CO_SUM);
+    k_reduce_chunks<<<1, kBlock, 0, C.stream>>>(C.cpart, nch, (size_t)nch, n, C.tres);
+    C.check_launch();
+  }
   C.phase_end();
   bool contact = contact_active(C);
   if (contact && C.ncand < 0) {
@@ -410,6 +451,7 @@ void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
   collect(C);
   const int npairs_x = C.npairs;  // pairs at the sweep-start x
   const bool gs = C.mode == 1 && C.color_ptr.size() > 1;
+  if (gs && C.partitioned) throw Error(JGS2_E_ARG, "the partitioned solve runs Jacobi sweeps only");
   int gs_acts = 0;
   double gs_gradsq = 0.0;
   if (gs) {
@@ -425,6 +467,8 @@ void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
                                                             guard ? 1 : 0, C.max_halvings,
                                                             C.alpha_floor, C.dx);
     C.check_launch();
+    // dx: each rank holds its own vertices' rows (zeros elsewhere)
+    C.allreduce(C.dx, 3 * (size_t)C.nv, CT_F64, CO_SUM);
     C.phase_end();
   }
   double gamma = 1.0, energy = 0.0, cap_used = 1.0;
@@ -524,10 +568,14 @@ void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
   }
   JGS2_CUDA(cudaMemcpyAsync(C.h_res, C.res, R_NSLOTS * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
   int n_indef = 0;
-  if (C.nuniq > 0)
+  if (C.partitioned) {
+    if (C.nuniq == 0) JGS2_CUDA(cudaMemsetAsync(C.hess_count, 0, sizeof(int), C.stream));
+    C.allreduce(C.hess_count, 1, CT_I32, CO_SUM);
+  }
+  if (C.nuniq > 0 || C.partitioned)
     JGS2_CUDA(cudaMemcpyAsync(C.h_res + R_NSLOTS + 1, C.hess_count, sizeof(int), cudaMemcpyDeviceToHost, C.stream));
   C.sync();
-  if (C.nuniq > 0) memcpy(&n_indef, C.h_res + R_NSLOTS + 1, sizeof(int));
+  if (C.nuniq > 0 || C.partitioned) memcpy(&n_indef, C.h_res + R_NSLOTS + 1, sizeof(int));
   if (info) {
     info->line_search_activations = guard ? acts_ls + halvings : 0;
     info->n_indefinite = n_indef;
@@ -591,6 +639,108 @@ jgs2_ctx* jgs2_create(int32_t device) {
     return nullptr;
   }
   return ctx;
+}
+
+jgs2_ctx* jgs2_create_on_stream(int32_t device, void* stream) {
+  jgs2_ctx* ctx = jgs2_create(device);
+  if (ctx && stream) {  // run on the caller's stream (not destroyed with the context)
+    cudaStreamSynchronize(ctx->c.stream);
+    cudaStreamDestroy(ctx->c.stream);
+    ctx->c.stream = static_cast<cudaStream_t>(stream);
+    ctx->c.own_stream = false;
+  }
+  return ctx;
+}
+
+int32_t jgs2_nccl_unique_id(uint8_t* id128) {
+  if (!id128) return JGS2_E_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return JGS2_E_CUDA;
+  static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(id128, &id, sizeof(id));
+  return JGS2_OK;
+}
+
+namespace {
+void check_comm_args(Ctx& C, int32_t world, int32_t rank) {
+  if (world < 1 || rank < 0 || rank >= world) throw Error(JGS2_E_ARG, "invalid world/rank");
+  if (C.comm) throw Error(JGS2_E_ARG, "communicator already set");
+  if (C.fac.ready || C.have_pre) throw Error(JGS2_E_ARG, "set the communicator before the factor and precompute");
+}
+}  // namespace
+
+int32_t jgs2_set_comm_nccl(jgs2_ctx* ctx, int32_t world, int32_t rank, const uint8_t* id128) {
+  return guarded(ctx, [&](Ctx& C) {
+    check_comm_args(C, world, rank);
+    if (!id128) throw Error(JGS2_E_ARG, "null unique id");
+    ncclUniqueId id;
+    memcpy(&id, id128, sizeof(id));
+    auto* nc = new NcclComm();
+    nc->rank = rank;
+    nc->world = world;
+    nc->owned = true;
+    ncclResult_t r = ncclCommInitRank(&nc->c, world, id, rank);
+    if (r != ncclSuccess) {
+      delete nc;
+      throw Error(JGS2_E_CUDA, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+    C.comm = nc;
+  });
+}
+
+int32_t jgs2_set_comm_nccl_handle(jgs2_ctx* ctx, int32_t world, int32_t rank, void* nccl_comm) {
+  return guarded(ctx, [&](Ctx& C) {
+    check_comm_args(C, world, rank);
+    if (!nccl_comm) throw Error(JGS2_E_ARG, "null ncclComm_t");
+    auto* nc = new NcclComm();
+    nc->rank = rank;
+    nc->world = world;
+    nc->c = static_cast<ncclComm_t>(nccl_comm);
+    C.comm = nc;
+  });
+}
+
+int32_t jgs2_set_comm_host(jgs2_ctx* ctx, int32_t world, int32_t rank, jgs2_allreduce_fn fn, void* user) {
+  return guarded(ctx, [&](Ctx& C) {
+    check_comm_args(C, world, rank);
+    if (!fn) throw Error(JGS2_E_ARG, "null all-reduce callback");
+    auto* hc = new HostComm();
+    hc->rank = rank;
+    hc->world = world;
+    hc->fn = fn;
+    hc->user = user;
+    C.comm = hc;
+  });
+}
+
+int32_t jgs2_set_partition(jgs2_ctx* ctx, int64_t v_begin, int64_t v_end) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (!C.have_model) throw Error(JGS2_E_ARG, "set the model first");
+    if (C.fac.ready || C.have_pre) throw Error(JGS2_E_ARG, "set the partition before the factor and precompute");
+    if (C.mode != 0) throw Error(JGS2_E_ARG, "the partitioned solve runs Jacobi sweeps only");
+    auto bv = std::find(C.body_v.begin(), C.body_v.end(), (int)v_begin);
+    auto ev = std::find(C.body_v.begin(), C.body_v.end(), (int)v_end);
+    if (v_begin < 0 || v_end > C.nv || v_begin >= v_end || bv == C.body_v.end() || ev == C.body_v.end())
+      throw Error(JGS2_E_ARG, "partition must cover whole bodies (vertex ids at body boundaries)");
+    int b0 = (int)(bv - C.body_v.begin()), b1 = (int)(ev - C.body_v.begin());
+    C.own_v0 = (int)v_begin;
+    C.own_v1 = (int)v_end;
+    C.own_e0 = C.body_e[b0];
+    C.own_e1 = C.body_e[b1];
+    C.chunk_own0 = C.chunk_first_e[b0];
+    C.chunk_own1 = C.chunk_first_e[b1];
+    C.vchunk_own0 = C.chunk_first_v[b0];
+    C.vchunk_own1 = C.chunk_first_v[b1];
+    std::vector<int> freel;
+    for (int v = C.own_v0; v < C.own_v1; ++v)
+      if (!C.h_fixed[v]) freel.push_back(v);
+    C.nfree = (int)freel.size();
+    C.free_list = C.upload(freel.data(), std::max<size_t>(freel.size(), 1));
+    C.partitioned = C.own_v0 != 0 || C.own_v1 != C.nv || (C.comm && C.comm->world > 1);
+    // rotations of other ranks' vertices stay zero (jgs2_get_rotations sums)
+    JGS2_CUDA(cudaMemsetAsync(C.R, 0, 9 * (size_t)C.nv * sizeof(double), C.stream));
+    C.sync();
+  });
 }
 
 void jgs2_destroy(jgs2_ctx* ctx) {
@@ -658,6 +808,56 @@ int32_t jgs2_set_model(jgs2_ctx* ctx, const jgs2_model* md) {
     JGS2_CUDA(cudaMemsetAsync(C.delta, 0, 3 * (size_t)nv * sizeof(double), C.stream));
     JGS2_CUDA(cudaMemsetAsync(C.dx, 0, 3 * (size_t)nv * sizeof(double), C.stream));
     contact_setup(C, md);
+    // body boundaries (bodies are numbered consecutively in vertex and element
+    // ids, as Model concatenates them, assembly.py:40-116) and the chunk table
+    C.body_v.assign(1, 0);
+    C.body_e.assign(1, 0);
+    bool monotone = md->vertex_body != nullptr;
+    for (int v = 1; v < nv && monotone; ++v) monotone = md->vertex_body[v] >= md->vertex_body[v - 1];
+    if (monotone) {
+      for (int v = 1; v < nv; ++v)
+        if (md->vertex_body[v] != md->vertex_body[v - 1]) C.body_v.push_back(v);
+      int b = 0;
+      for (int e = 0; e < ne; ++e) {  // first element of each body
+        int64_t eb = md->vertex_body[md->tets[4 * (size_t)e]];
+        while (b + 1 < (int)C.body_v.size() && eb >= md->vertex_body[C.body_v[b + 1]]) {
+          C.body_e.push_back(e);
+          ++b;
+        }
+        for (int a = 1; a < 4 && monotone; ++a) monotone = md->vertex_body[md->tets[4 * (size_t)e + a]] == eb;
+        if (e > 0 && eb < md->vertex_body[md->tets[4 * (size_t)(e - 1)]]) monotone = false;
+      }
+      while (C.body_e.size() < C.body_v.size()) C.body_e.push_back(ne);
+    }
+    if (!monotone) {  // one block: no partitioning possible
+      C.body_v.assign(1, 0);
+      C.body_e.assign(1, 0);
+    }
+    C.body_v.push_back(nv);
+    C.body_e.push_back(ne);
+    std::vector<int2> ch;
+    std::vector<int> ech_first(C.body_e.size()), vch_first(C.body_v.size());
+    for (size_t b = 0; b + 1 < C.body_e.size(); ++b) {
+      ech_first[b] = (int)ch.size();
+      for (int e = C.body_e[b]; e < C.body_e[b + 1]; e += kChunkE)
+        ch.push_back(make_int2(e, std::min(e + kChunkE, C.body_e[b + 1])));
+    }
+    ech_first.back() = (int)ch.size();
+    C.nchunk_e = (int)ch.size();
+    for (size_t b = 0; b + 1 < C.body_v.size(); ++b) {
+      vch_first[b] = (int)ch.size();
+      for (int v = C.body_v[b]; v < C.body_v[b + 1]; v += kChunkV)
+        ch.push_back(make_int2(v, std::min(v + kChunkV, C.body_v[b + 1])));
+    }
+    vch_first.back() = (int)ch.size();
+    C.nchunk_v = (int)ch.size() - C.nchunk_e;
+    C.chunk_first_e = ech_first;
+    C.chunk_first_v = vch_first;
+    C.chunks = C.upload(ch.data(), ch.size());
+    C.cpart = C.alloc<double>((size_t)(kTrials + 1) * ch.size());
+    C.own_v0 = 0; C.own_v1 = nv; C.own_e0 = 0; C.own_e1 = ne;
+    C.chunk_own0 = 0; C.chunk_own1 = C.nchunk_e;
+    C.vchunk_own0 = C.nchunk_e; C.vchunk_own1 = C.nchunk_e + C.nchunk_v;
     C.have_model = true;
     C.sync();
   });
@@ -675,6 +875,7 @@ int32_t jgs2_set_precompute(jgs2_ctx* ctx, const jgs2_precompute* p, const jgs2_
     C.max_halvings = cfg->max_halvings;
     C.alpha_floor = cfg->alpha_floor;
     if (cfg->mode != 0 && cfg->mode != 1) throw Error(JGS2_E_ARG, "mode must be 0 (jacobi) or 1 (gauss_seidel)");
+    if (cfg->mode != 0 && C.partitioned) throw Error(JGS2_E_ARG, "the partitioned solve runs Jacobi sweeps only");
     C.mode = cfg->mode;
     if (C.tol_dx <= 0 || C.max_outer < 1 || C.max_halvings < 0)
       throw Error(JGS2_E_ARG, "invalid solver config");
@@ -688,14 +889,14 @@ int32_t jgs2_set_precompute(jgs2_ctx* ctx, const jgs2_precompute* p, const jgs2_
       bidx[v] = (int)k;
     }
     for (int v = 0; v < nv; ++v)
-      if (!C.h_fixed[v] && bidx[v] < 0)
+      if (!C.h_fixed[v] && C.owns(v) && bidx[v] < 0)
         throw Error(JGS2_E_KEY, "free vertex " + std::to_string(v) + " has no basis");
     std::vector<double> gbar(9 * (size_t)nv, 0.0), grows(9 * (size_t)C.gmax * nv, 0.0);
     std::vector<int> group((size_t)C.gmax * nv, -1);
     int smax = 0;
     for (int v = 0; v < nv; ++v) {
       int k = bidx[v];
-      if (k < 0 || C.h_fixed[v]) continue;
+      if (k < 0 || C.h_fixed[v] || !C.owns(v)) continue;  // this rank's vertices
       smax = std::max<int>(smax, (int)(p->cub_ptr[k + 1] - p->cub_ptr[k]));
       for (int i = 0; i < 9; ++i) gbar[9 * (size_t)v + i] = p->gbar[9 * k + i];
       for (int g = 0; g < p->gmax; ++g) group[(size_t)C.gmax * v + g] = (int)p->group[p->gmax * k + g];
@@ -714,7 +915,7 @@ int32_t jgs2_set_precompute(jgs2_ctx* ctx, const jgs2_precompute* p, const jgs2_
     std::vector<int4> cub_verts(ns, make_int4(0, 0, 0, 0));
     for (int v = 0; v < nv; ++v) {
       int k = bidx[v];
-      if (k < 0 || C.h_fixed[v]) continue;
+      if (k < 0 || C.h_fixed[v] || !C.owns(v)) continue;  // this rank's vertices
       const int64_t* keys = p->vrows_keys + p->vrows_ptr[k];
       int64_t nk = p->vrows_ptr[k + 1] - p->vrows_ptr[k];
       for (int64_t s = p->cub_ptr[k]; s < p->cub_ptr[k + 1]; ++s) {
@@ -907,6 +1108,19 @@ int32_t jgs2_set_rotations(jgs2_ctx* ctx, const double* R) {
 
 int32_t jgs2_get_rotations(jgs2_ctx* ctx, double* R) {
   return guarded(ctx, [&](Ctx& C) {
+    if (C.partitioned) {  // each rank holds its own vertices' rotations: sum the slices
+      size_t n9 = 9 * (size_t)C.nv;
+      double* t = nullptr;
+      JGS2_CUDA(cudaMallocAsync(&t, n9 * sizeof(double), C.stream));
+      JGS2_CUDA(cudaMemsetAsync(t, 0, n9 * sizeof(double), C.stream));
+      size_t o = 9 * (size_t)C.own_v0, n = 9 * (size_t)(C.own_v1 - C.own_v0);
+      JGS2_CUDA(cudaMemcpyAsync(t + o, C.R + o, n * sizeof(double), cudaMemcpyDeviceToDevice, C.stream));
+      C.allreduce(t, n9, CT_F64, CO_SUM);
+      JGS2_CUDA(cudaMemcpyAsync(R, t, n9 * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+      JGS2_CUDA(cudaFreeAsync(t, C.stream));
+      C.sync();
+      return;
+    }
     JGS2_CUDA(cudaMemcpyAsync(R, C.R, 9 * (size_t)C.nv * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
     C.sync();
   });

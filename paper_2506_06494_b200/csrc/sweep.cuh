@@ -20,6 +20,7 @@ struct DevModel {
   const uint8_t* fixed;
   const int* pos;
   const int* free_list;
+  int v0, v1;  // this rank's vertex range (vertex pass)
 };
 
 // ---------------------------------------------------------------- vertex pass
@@ -33,8 +34,8 @@ template <bool ROT>
 __global__ void __launch_bounds__(kBlock)
 k_vertex_pass(DevModel m, const double* __restrict__ x, const double* __restrict__ z, double h,
               double* __restrict__ R, double* __restrict__ gasm) {
-  int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= m.nv) return;
+  int v = m.v0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= m.v1) return;
   double h2 = h * h;
   double xv[3] = {x[3 * v], x[3 * v + 1], x[3 * v + 2]};
   double dv[3];
@@ -93,22 +94,18 @@ k_vertex_pass(DevModel m, const double* __restrict__ x, const double* __restrict
   }
 }
 
-// y = R^T g into ND-ordered rhs for free vertices; grad_sq reduction
-// (local_solver.py:124-125, 602-603).
+// y = R^T g into the ND-ordered rhs for free vertices (local_solver.py:124-125);
+// grad_sq is reduced in vertex chunks (partition.cuh)
 __global__ void __launch_bounds__(kBlock)
-k_rhs(DevModel m, const double* __restrict__ R, const double* __restrict__ gasm, double* b,
-      double* partials, unsigned* counter, double* out) {
-  double gs = 0.0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m.nfree; i += gridDim.x * blockDim.x) {
-    int v = m.free_list[i];
-    double g[3] = {gasm[3 * v], gasm[3 * v + 1], gasm[3 * v + 2]};
-    double y[3];
-    mat3_tvec(R + 9 * (size_t)v, g, y);
-    int p = m.pos[v];
-    b[3 * p] = y[0]; b[3 * p + 1] = y[1]; b[3 * p + 2] = y[2];
-    gs += g[0] * g[0] + g[1] * g[1] + g[2] * g[2];
-  }
-  grid_reduce<OP_SUM>(gs, partials, counter, out);
+k_rhs(DevModel m, const double* __restrict__ R, const double* __restrict__ gasm, double* b) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m.nfree) return;
+  int v = m.free_list[i];
+  double g[3] = {gasm[3 * v], gasm[3 * v + 1], gasm[3 * v + 2]};
+  double y[3];
+  mat3_tvec(R + 9 * (size_t)v, g, y);
+  int p = m.pos[v];
+  b[3 * p] = y[0]; b[3 * p + 1] = y[1]; b[3 * p + 2] = y[2];
 }
 
 // q lookup in the ND-ordered solution (fixed vertices: q = 0)

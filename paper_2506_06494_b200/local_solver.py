@@ -142,14 +142,18 @@ class LocalSolver:
     """GPU JGS2 solver with the reference ``LocalSolver`` interface.
 
     ``factor`` may be the reference's SuperLU rest factorization (the matrix
-    it factored is rebuilt and refactored on the device), a float ``h_ref``,
-    or ``None`` together with ``h_ref=`` / ``hbar=`` keywords. ``precompute``
-    (a :class:`~paper_2506_06494_b200.precompute.Precompute`) may replace
-    ``bases``/``cubature_sets``.
+    it factored is recovered on the mesh pattern and refactored on the
+    device), a float ``h_ref``, or ``None`` together with ``h_ref=`` /
+    ``hbar=`` keywords (``hbar=RuntimeData.hbar`` passes the reference's
+    own matrix, harness.py:29-35). ``precompute`` (a
+    :class:`~paper_2506_06494_b200.precompute.Precompute`) may replace
+    ``bases``/``cubature_sets``. ``dist`` (torch.distributed, world > 1)
+    partitions the scene by bodies across the ranks' GPUs (partition.py).
     """
 
     def __init__(self, model, config, bases=None, cubature_sets=None, factor=None, *,
-                 precompute=None, h_ref=None, hbar=None, device=0, leaf_size=32):
+                 precompute=None, h_ref=None, hbar=None, device=0, leaf_size=32, dist=None,
+                 comm="nccl"):
         self.model = model
         self.config = config
         if config.subspace != "corotated_cubature":
@@ -179,6 +183,15 @@ class LocalSolver:
             raise RuntimeError(f"jgs2_create failed on device {device}")
         self._keep = []
         self._upload_model(model)
+        # partitioned solve (partition.py): dist = an initialized
+        # torch.distributed with world > 1, one rank per GPU; comm = "nccl" or
+        # "host" (gloo callback, for ranks sharing a GPU in tests)
+        self.partition, self._comm_keep = None, None
+        if dist is not None and dist.get_world_size() > 1:
+            from . import partition as P
+            self._comm_keep = P.attach(self._lib, self._ctx, dist, comm)
+            self.partition = P.plan(model, dist.get_world_size())[dist.get_rank()]
+            self._call(self._lib.jgs2_set_partition, int(self.partition[0]), int(self.partition[1]))
         t0 = time.perf_counter()
         self.factor_info = L.FactorInfo()
         if hbar is not None:
@@ -233,6 +246,8 @@ class LocalSolver:
             d.surface_tri_body = L.ptr(arr(m.surface_tri_body, L.i64a), L.i64)
         else:
             d.n_bodies = len(getattr(m, "bodies", [0]))
+            if getattr(m, "vertex_body", None) is not None:
+                d.vertex_body = L.ptr(arr(m.vertex_body, L.i64a), L.i64)
         self._call(self._lib.jgs2_set_model, C_ref(d))
 
     def _upload_precompute(self, p, cfg):
