@@ -313,6 +313,7 @@ def main():
         "mean_gamma_over_cap_accepted": (float(np.mean([r["gamma"] / r["cap"] for r, a in zip(record, accepted)
                                                         if a and r["cap"] > 0])) if accepted.any() else None),
         "mean_pairs": float(np.mean([r["n_pairs"] for r in record])),
+        "mean_indefinite_elements": float(np.mean([r["n_indefinite"] for r in record])),
     }
 
     # roofline of the dominant HBM-modelled kernel (3x3-block arithmetic +

@@ -19,6 +19,8 @@
 // M+ = Q max(L, 0) Q^T. Divisions and square roots use the FP64-pipe
 // Newton forms of dmath.cuh (the MUFU.*64H forms saturated the XU pipe).
 #pragma once
+#include <algorithm>
+
 #include "dmath.cuh"
 #include "physics.cuh"
 
@@ -280,14 +282,342 @@ __device__ __forceinline__ void sym_eig9_reg(double* V, double (&d)[9], double (
 #undef VV
 }
 
+// Pass 1, one thread per element: closed-form M (written to the element's
+// slot), the LDL^T inertia test, and the indefinite elements compacted into
+// `list` (warp-aggregated atomic; the order of the list does not affect any
+// result, each element owns its output slot).
+__global__ void __launch_bounds__(kHessThreads)
+k_mplus_closed(int n, const int* elems, const double* __restrict__ xs, const int4* __restrict__ tets,
+               const double* __restrict__ dminv, const double4* __restrict__ eprops, double* mplus, int* count,
+               int* list) {
+  // the block's 128 x 45 outputs are staged in shared memory and stored
+  // contiguously (per-thread 360-B strided stores were lg-throttle bound)
+  __shared__ double stage[kHessThreads * 45];
+  int u = blockIdx.x * blockDim.x + threadIdx.x;
+  bool indef = false;
+  if (u < n) {
+    int e = elems ? elems[u] : u;
+    double D[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) D[i] = __ldg(dminv + 9 * (size_t)e + i);
+    int4 t = __ldg(tets + e);
+    double x0[3], x1[3], x2[3], x3[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      x0[c] = __ldg(xs + 3 * t.x + c); x1[c] = __ldg(xs + 3 * t.y + c);
+      x2[c] = __ldg(xs + 3 * t.z + c); x3[c] = __ldg(xs + 3 * t.w + c);
+    }
+    double F[9];
+    deformation_gradient(x0, x1, x2, x3, D, F);
+    double4 ep = eprops[e];
+    double Mp[45];
+    reduced_hessian_closed(F, D, ep.x, snh_const(ep.y, ep.z), Mp);
+#pragma unroll
+    for (int i = 0; i < 45; ++i) stage[45 * threadIdx.x + i] = Mp[i];
+    indef = !is_pos_def9(Mp);
+  }
+  __syncthreads();
+  const int base = blockIdx.x * blockDim.x;
+  const int cnt = 45 * min((int)blockDim.x, n - base);
+  double* o = mplus + 45 * (size_t)base;
+  for (int k = threadIdx.x; k < cnt; k += blockDim.x) o[k] = stage[k];
+  unsigned ball = __ballot_sync(0xffffffffu, indef);
+  int lane = threadIdx.x & 31, b0 = 0;
+  if (lane == 0 && ball) b0 = atomicAdd(count, __popc(ball));
+  b0 = __shfl_sync(0xffffffffu, b0, 0);
+  if (indef) list[b0 + __popc(ball & ((1u << lane) - 1u))] = u;
+}
+
+// ---- negative-eigenspace projection (pass 2)
+//
+// M+ = Q max(L, 0) Q^T = M - sum_{l_j < 0} l_j q_j q_j^T: only the negative
+// eigenpairs are needed (typically 1-3 of 9). Householder reduction
+// M = Q T Q^T (Numerical Recipes tred2 order, reflectors kept in the packed
+// lower triangle), eigenvalues of T by implicit QL without vectors, then per
+// negative eigenvalue inverse iteration on T (guarded LDL^T), Gram-Schmidt
+// against the previous ones (clustered spectra), and the back-transform
+// q = H_{n-1} ... H_1 y. More than kNegMax negative eigenvalues fall back to
+// the full tred2/tql2 eigendecomposition.
+constexpr int kNegMax = 4;
+#ifndef JGS2_PROJ_MINBLOCKS
+#define JGS2_PROJ_MINBLOCKS 2
+#endif
+#ifndef JGS2_HESS_MINBLOCKS
+#define JGS2_HESS_MINBLOCKS 2
+#endif
+#define JGS2_A(i, j) A[JGS2_PK(i, j) * S]
+
+template <int S>
+__device__ __forceinline__ void tred9_packed(double* A, double (&d)[9], double (&e)[9], double (&hv)[9]) {
+  constexpr int n = 9;
+#pragma unroll
+  for (int i = n - 1; i > 0; --i) {
+    const int l = i - 1;
+    double h = 0.0;
+    if (l > 0) {
+      double scale = 0.0;
+#pragma unroll
+      for (int k = 0; k <= l; ++k) scale += fabs(JGS2_A(i, k));
+      if (scale == 0.0) {
+        e[i] = JGS2_A(i, l);
+      } else {
+        const double rs = rcp_nr(scale);
+#pragma unroll
+        for (int k = 0; k <= l; ++k) {
+          double v = JGS2_A(i, k) * rs;
+          JGS2_A(i, k) = v;
+          h += v * v;
+        }
+        double f = JGS2_A(i, l);
+        double g = sqrt_nr(h);
+        if (f >= 0.0) g = -g;
+        e[i] = scale * g;
+        h -= f * g;
+        JGS2_A(i, l) = f - g;
+        const double rh = rcp_nr(h);
+        f = 0.0;
+#pragma unroll
+        for (int j = 0; j <= l; ++j) {
+          double gg = 0.0;
+#pragma unroll
+          for (int k = 0; k <= j; ++k) gg += JGS2_A(j, k) * JGS2_A(i, k);
+#pragma unroll
+          for (int k = j + 1; k <= l; ++k) gg += JGS2_A(k, j) * JGS2_A(i, k);
+          e[j] = gg * rh;
+          f += e[j] * JGS2_A(i, j);
+        }
+        const double hh = f * 0.5 * rh;
+#pragma unroll
+        for (int j = 0; j <= l; ++j) {
+          f = JGS2_A(i, j);
+          const double gg = e[j] - hh * f;
+          e[j] = gg;
+#pragma unroll
+          for (int k = 0; k <= j; ++k) JGS2_A(j, k) -= (f * e[k] + gg * JGS2_A(i, k));
+        }
+      }
+    } else {
+      e[i] = JGS2_A(i, l);
+    }
+    hv[i] = h;
+  }
+  hv[0] = 0.0;
+  e[0] = 0.0;
+#pragma unroll
+  for (int i = 0; i < n; ++i) d[i] = JGS2_A(i, i);
+}
+
+// eigenvalues of the symmetric tridiagonal T (diagonal d, T(i, i-1) = e[i])
+// in place in d (implicit QL, JAMA tql2 without the vector updates)
+__device__ __forceinline__ void tql1_9(double (&d)[9], double (&e)[9]) {
+  constexpr int n = 9;
+#pragma unroll
+  for (int i = 1; i < n; ++i) e[i - 1] = e[i];
+  e[n - 1] = 0.0;
+  double f = 0.0, tst1 = 0.0;
+  const double eps = 2.220446049250313e-16;
+#pragma unroll
+  for (int l = 0; l < n; ++l) {
+    tst1 = fmax(tst1, fabs(d[l]) + fabs(e[l]));
+    int m = n - 1;
+#pragma unroll
+    for (int mm = n - 2; mm >= l; --mm)
+      if (fabs(e[mm]) <= eps * tst1) m = mm;
+    if (l < n - 1 && m > l) {
+      int iter = 0;
+      do {
+        ++iter;
+        double g = d[l];
+        double p = div_nr(d[l + 1] - g, 2.0 * e[l]);
+        double r = sqrt_nr(fma(p, p, 1.0));
+        if (p < 0) r = -r;
+        d[l] = div_nr(e[l], p + r);
+        d[l + 1] = e[l] * (p + r);
+        double dl1 = d[l + 1];
+        double h = g - d[l];
+#pragma unroll
+        for (int i = l + 2; i < n; ++i) d[i] -= h;
+        f += h;
+        p = d[n - 1];
+#pragma unroll
+        for (int i = n - 2; i > l; --i)
+          if (i == m) p = d[i];
+        double c = 1.0, c2 = c, c3 = c;
+        double el1 = e[l + 1];
+        double s = 0.0, s2 = 0.0;
+#pragma unroll
+        for (int i = n - 2; i >= l; --i) {
+          if (i < m) {
+            c3 = c2;
+            c2 = c;
+            s2 = s;
+            g = c * e[i];
+            h = c * p;
+            double ei = e[i];
+            double q2 = fma(p, p, ei * ei);
+            double ri = rsqrt_nr(q2);
+            r = sqrt_from_rsqrt(q2, ri);
+            e[i + 1] = s * r;
+            s = ei * ri;
+            c = p * ri;
+            p = c * d[i] - s * g;
+            d[i + 1] = h + s * (c * g + s * d[i]);
+          }
+        }
+        p = div_nr(-s * s2 * c3 * el1 * e[l], dl1);
+        e[l] = s * p;
+        d[l] = c * p;
+      } while (fabs(e[l]) > eps * tst1 && iter < 60);
+    }
+    d[l] = d[l] + f;
+    e[l] = 0.0;
+  }
+}
+
+// y <- normalized solution of (T - lam I) y = y (3 steps), T = (d, e), guarded
+// LDL^T without pivoting (near-singular by construction)
+__device__ __forceinline__ void inverse_iteration9(const double (&d)[9], const double (&e)[9], double lam,
+                                                   double tnorm, double (&y)[9]) {
+  constexpr int n = 9;
+  const double tiny = 2.220446049250313e-16 * tnorm + 1e-300;
+  double Lo[9], Di[9];
+  double Dk = d[0] - lam;
+  if (fabs(Dk) < tiny) Dk = tiny;
+  Lo[0] = 0.0;
+  Di[0] = rcp_nr(Dk);
+#pragma unroll
+  for (int k = 1; k < n; ++k) {
+    Lo[k] = e[k] * Di[k - 1];
+    Dk = (d[k] - lam) - Lo[k] * e[k];
+    if (fabs(Dk) < tiny) Dk = tiny;
+    Di[k] = rcp_nr(Dk);
+  }
+#pragma unroll 1
+  for (int it = 0; it < 3; ++it) {
+#pragma unroll
+    for (int k = 1; k < n; ++k) y[k] -= Lo[k] * y[k - 1];
+#pragma unroll
+    for (int k = 0; k < n; ++k) y[k] *= Di[k];
+#pragma unroll
+    for (int k = n - 2; k >= 0; --k) y[k] -= Lo[k + 1] * y[k + 1];
+    double nn = 0.0;
+#pragma unroll
+    for (int k = 0; k < n; ++k) nn += y[k] * y[k];
+    const double rn = rsqrt_nr(nn);
+#pragma unroll
+    for (int k = 0; k < n; ++k) y[k] *= rn;
+  }
+}
+
+// Pass 2 over the compacted indefinite elements (grid-stride up to *count):
+// M+ written over M in place.
+__global__ void __launch_bounds__(kHessThreads, JGS2_PROJ_MINBLOCKS)
+k_mplus_project(int* count, const int* list, int* list2, double* mplus) {
+  extern __shared__ double hsm[];
+  constexpr int S = kHessThreads;
+  const int n = *count;
+  for (int i0 = blockIdx.x * blockDim.x; i0 < n; i0 += gridDim.x * blockDim.x) {
+    int idx = i0 + threadIdx.x;
+    if (idx >= n) break;
+    double* o = mplus + 45 * (size_t)list[idx];
+    double* A = hsm + threadIdx.x;              // packed lower 45 (reflectors after tred)
+    double* Y = hsm + 45 * S + threadIdx.x;     // kNegMax - 1 tridiagonal-space vectors
+    double* Tm = hsm + (45 + 9 * (kNegMax - 1)) * S + threadIdx.x;  // T: diagonal, subdiagonal
+    double tnorm = 0.0;
+#pragma unroll
+    for (int q = 0; q < 45; ++q) {
+      double m = o[q];
+      A[q * S] = m;
+      tnorm = fmax(tnorm, fabs(m));
+    }
+    double lam[9], ee[9];
+    {
+      double hv[9];
+      tred9_packed<S>(A, lam, ee, hv);
+#pragma unroll
+      for (int i = 0; i < 9; ++i) {
+        JGS2_A(i, i) = hv[i];  // reflector norms h_i in the (now unused) diagonal slots
+        Tm[i * S] = lam[i];
+        Tm[(9 + i) * S] = ee[i];
+      }
+    }
+    tql1_9(lam, ee);
+    // negative eigenvalues, ascending (at most 9; selection into neg[])
+    int k = 0;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) k += lam[q] < 0.0;
+    if (k == 0) continue;  // PSD already (LDL^T failed on a zero pivot)
+    if (k > kNegMax) {  // many negative modes: the full eigendecomposition (k_mplus_full)
+      int slot = atomicAdd(count + 1, 1);
+      list2[slot] = list[idx];
+      continue;
+    }
+#pragma unroll 1
+    for (int j = 0; j < k; ++j) {
+      double l = 0.0;  // j-th smallest eigenvalue (negative), removed from lam
+#pragma unroll
+      for (int q = 0; q < 9; ++q) l = fmin(l, lam[q]);
+      bool done = false;
+#pragma unroll
+      for (int q = 0; q < 9; ++q)
+        if (!done && lam[q] == l) { lam[q] = 0.0; done = true; }
+      double y[9];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) y[q] = 1.0 + 0.1 * q + 0.01 * j * q * q;
+      {
+        double d[9], e[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) { d[q] = Tm[q * S]; e[q] = Tm[(9 + q) * S]; }
+        inverse_iteration9(d, e, l, tnorm, y);
+      }
+#pragma unroll 1
+      for (int t = 0; t < j; ++t) {  // Gram-Schmidt against earlier negative vectors
+        const double* Yt = Y + 9 * t * S;
+        double dp = 0.0;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) dp += Yt[q * S] * y[q];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) y[q] -= dp * Yt[q * S];
+      }
+      double nn = 0.0;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) nn += y[q] * y[q];
+      const double rn = rsqrt_nr(nn);
+#pragma unroll
+      for (int q = 0; q < 9; ++q) y[q] *= rn;
+      if (j < kNegMax - 1) {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) Y[(9 * j + q) * S] = y[q];
+      }
+      // back-transform q = H_8 ... H_1 y, H_i = I - u_i u_i^T / h_i, u_i = A(i, 0..i-1)
+#pragma unroll
+      for (int i = 1; i < 9; ++i) {
+        const double hi = JGS2_A(i, i);
+        if (hi != 0.0) {
+          double dp = 0.0;
+#pragma unroll
+          for (int c = 0; c < i; ++c) dp += JGS2_A(i, c) * y[c];
+          dp *= rcp_nr(hi);
+#pragma unroll
+          for (int c = 0; c < i; ++c) y[c] -= dp * JGS2_A(i, c);
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 9; ++a)
+#pragma unroll
+        for (int b = 0; b <= a; ++b) o[JGS2_PK(a, b)] -= l * y[a] * y[b];
+    }
+  }
+}
+#undef JGS2_A
+
+// One-pass form (JGS2_HESS_ONEPASS=1, for A/B measurements): the full
+// eigendecomposition for every indefinite element of a warp.
 // One thread per element: closed-form M, LDL^T inertia test, and (when
 // indefinite) the tred2/tql2 projection on per-thread interleaved shared
 // memory. The number of indefinite elements is accumulated with one
 // warp-aggregated atomic per warp (diagnostic only; results do not depend
 // on it).
-#ifndef JGS2_HESS_MINBLOCKS
-#define JGS2_HESS_MINBLOCKS 2
-#endif
 __global__ void __launch_bounds__(kHessThreads, JGS2_HESS_MINBLOCKS)
 k_element_mplus(int n, const int* elems, const double* __restrict__ xs, const int4* __restrict__ tets,
                 const double* __restrict__ dminv, const double4* __restrict__ eprops, double* mplus,
@@ -351,16 +681,74 @@ k_element_mplus(int n, const int* elems, const double* __restrict__ xs, const in
   if ((threadIdx.x & 31) == 0 && ball) atomicAdd(count, __popc(ball));
 }
 constexpr size_t kHessSmemBytes = 81 * kHessThreads * sizeof(double);
+constexpr size_t kProjSmemBytes = (45 + 9 * (kNegMax - 1) + 18) * kHessThreads * sizeof(double);
 
-// count: device int, zeroed here; list: unused (kept for the call sites).
+// Pass 3: the rare elements with more than kNegMax negative modes, full
+// tred2/tql2 eigendecomposition (grid-stride up to count[1]).
+__global__ void __launch_bounds__(kHessThreads, 2)
+k_mplus_full(const int* count, const int* list2, double* mplus) {
+  extern __shared__ double hsm[];
+  constexpr int S = kHessThreads;
+  const int n = count[1];
+  for (int i0 = blockIdx.x * blockDim.x; i0 < n; i0 += gridDim.x * blockDim.x) {
+    int idx = i0 + threadIdx.x;
+    if (idx >= n) break;
+    double* o = mplus + 45 * (size_t)list2[idx];
+    double* V = hsm + threadIdx.x;
+#pragma unroll
+    for (int a = 0; a < 9; ++a)
+#pragma unroll
+      for (int b = 0; b <= a; ++b) {
+        double m = o[JGS2_PK(a, b)];
+        V[(9 * a + b) * S] = m;
+        V[(9 * b + a) * S] = m;
+      }
+    double dg[9], od[9];
+    sym_eig9_reg<S>(V, dg, od);
+#pragma unroll
+    for (int q = 0; q < 9; ++q) dg[q] = fmax(dg[q], 0.0);
+#pragma unroll
+    for (int a = 0; a < 9; ++a) {
+      double vi[9];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) vi[q] = V[(9 * a + q) * S] * dg[q];
+#pragma unroll
+      for (int b = 0; b <= a; ++b) {
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) acc += vi[q] * V[(9 * b + q) * S];
+        o[JGS2_PK(a, b)] = acc;
+      }
+    }
+  }
+}
+
+// Projected reduced Hessians of n elements (elems[u], or u when null) into
+// out[45 u]: pass 1 for all, pass 2 for the indefinite ones only (about half
+// of the cubature elements in a deforming scene; a warp of the one-pass form
+// paid the eigen solve whenever any of its 32 elements needed it).
+// count: 2 device ints (zeroed here; count[0] = indefinite elements,
+// count[1] = those with more than kNegMax negative modes);
+// list: device scratch of 2n ints.
 inline void launch_element_mplus(int n, const int* elems, const double* xs, const int4* tets,
                                  const double* dminv, const double4* eprops, double* out, int* count,
-                                 int* /*list*/, cudaStream_t stream) {
+                                 int* list, cudaStream_t stream) {
   if (n <= 0) return;
   int grid = (n + kHessThreads - 1) / kHessThreads;
-  cudaMemsetAsync(count, 0, sizeof(int), stream);
-  k_element_mplus<<<grid, kHessThreads, kHessSmemBytes, stream>>>(n, elems, xs, tets, dminv, eprops, out,
-                                                                  count);
+  cudaMemsetAsync(count, 0, 2 * sizeof(int), stream);
+  static const bool onepass = getenv("JGS2_HESS_ONEPASS") != nullptr;
+  if (onepass) {
+    k_element_mplus<<<grid, kHessThreads, kHessSmemBytes, stream>>>(n, elems, xs, tets, dminv, eprops, out,
+                                                                    count);
+    return;
+  }
+  k_mplus_closed<<<grid, kHessThreads, 0, stream>>>(n, elems, xs, tets, dminv, eprops, out, count, list);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int grid2 = std::min(grid, sms * JGS2_HESS_MINBLOCKS * 4);
+  k_mplus_project<<<std::min(grid, sms * 3 * 4), kHessThreads, kProjSmemBytes, stream>>>(count, list, list + n,
+                                                                                        out);
+  k_mplus_full<<<grid2, kHessThreads, kHessSmemBytes, stream>>>(count, list + n, out);
 }
 
 }  // namespace jgs2

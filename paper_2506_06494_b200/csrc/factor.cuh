@@ -583,7 +583,7 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
   if (!blocks) {
     JGS2_CUDA(cudaMallocAsync(&mp_all, 45 * (size_t)std::max(ne, 1) * sizeof(double), C.stream));
     int* tmp_list = nullptr;
-    JGS2_CUDA(cudaMallocAsync(&tmp_list, (size_t)std::max(ne, 1) * sizeof(int), C.stream));
+    JGS2_CUDA(cudaMallocAsync(&tmp_list, 2 * (size_t)std::max(ne, 1) * sizeof(int), C.stream));
     launch_element_mplus(ne, nullptr, C.rest, C.tets, C.dminv, C.eprops, mp_all, C.hess_count, tmp_list,
                          C.stream);
     C.launches += 1;

@@ -179,7 +179,7 @@ void hessians_async(Ctx& C) {
   }
   launch_element_mplus(C.nuniq, C.uniq, C.x, C.tets, C.dminv, C.eprops, C.mplus, C.hess_count,
                        C.hess_list, C.stream2);
-  C.launches += 1;
+  C.launches += 3;
   C.check_launch();
   if (C.profiling) {
     cudaEvent_t b = C.take_event();
@@ -631,6 +631,10 @@ jgs2_ctx* jgs2_create(int32_t device) {
     JGS2_CUDA(cudaStreamCreateWithPriority(&C.stream2, cudaStreamNonBlocking, prio_lo));
     JGS2_CUDA(cudaEventCreateWithFlags(&C.ev_fork, cudaEventDisableTiming));
     JGS2_CUDA(cudaEventCreateWithFlags(&C.ev_join, cudaEventDisableTiming));
+    cudaFuncSetAttribute(k_mplus_project, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kProjSmemBytes);
+    cudaFuncSetAttribute(k_mplus_full, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kHessSmemBytes);
     cudaFuncSetAttribute(k_element_mplus, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kHessSmemBytes);
 
@@ -956,7 +960,7 @@ int32_t jgs2_set_precompute(jgs2_ctx* ctx, const jgs2_precompute* p, const jgs2_
     C.nslots = 0;
     for (int e : cub_e) C.nslots += (e >= 0);
     C.mplus = C.alloc<double>(45 * (size_t)std::max(C.nuniq, 1));
-    C.hess_list = C.alloc<int>(std::max(C.nuniq, 1));
+    C.hess_list = C.alloc<int>(2 * (size_t)std::max(C.nuniq, 1));
     C.crest = C.alloc<double>(9 * (size_t)nv);
     JGS2_CUDA(cudaMemsetAsync(C.crest, 0, 9 * (size_t)nv * sizeof(double), C.stream));
     C.ls_max = C.alloc<unsigned long long>(C.max_halvings + 2);
