@@ -256,6 +256,41 @@ int32_t jgs2_set_partition(jgs2_ctx* ctx, int64_t v_begin, int64_t v_end);
 /* context on a caller-provided CUDA stream (cudaStream_t; NULL = own) */
 jgs2_ctx* jgs2_create_on_stream(int32_t device, void* stream);
 
+/* ---- scalable precompute (replaces harness.prepare's
+ * subspace.precompute_bases + retain_rows + cubature.train_all,
+ * harness.py:57-107, subspace.py:133-203, cubature.py:113-291) ------------
+ * Call order on a context with the model set and the rest factor built
+ * (jgs2_factor_rest): jgs2_selected_inverse -> (training inputs) ->
+ * jgs2_precompute_train -> jgs2_precompute_export. */
+/* Hbar^-1 on the factor's pattern (Takahashi equations, cuBLAS per front) */
+int32_t jgs2_selected_inverse(jgs2_ctx* ctx, double* seconds);
+/* (Hbar^-1)_{w v} 3x3 blocks (row-major) for n vertex pairs; found[k] = 0
+ * when (v, w) is not adjacent in the filled graph */
+int32_t jgs2_inverse_blocks(jgs2_ctx* ctx, int64_t n, const int64_t* v, const int64_t* w, double* out,
+                            int32_t* found);
+/* element stencil gradients at x (cubature.stencil_gradients,
+ * cubature.py:37-60): out[ne*12], vertex-major element DOFs */
+int32_t jgs2_stencil_gradients(jgs2_ctx* ctx, const double* x, const double* z, double h, double* out);
+typedef struct jgs2_train_params {
+  int32_t n_poses;              /* T training poses (cubature.build_training_set) */
+  int32_t candidates_per_round; /* 32 */
+  int32_t max_size;             /* 6 */
+  int32_t pad_;
+  double target_residual;       /* 0.01 */
+  uint64_t seed;
+  const double* pose_grads;     /* T*ne*12 stencil gradients per pose */
+  const double* pose_solves;    /* T*nv*3: Hbar^-1 applied to each pose's assembled gradient */
+} jgs2_train_params;
+/* bases + cubature sets of every free vertex; sizes = [n_bases, retained
+ * rows, cubature elements] */
+int32_t jgs2_precompute_train(jgs2_ctx* ctx, const jgs2_train_params* params, int64_t* sizes);
+/* the jgs2_precompute layout (gbar_rows = gbar, group = the vertex; Jacobi
+ * sub-problems, harness.py:66-69) plus per-vertex training residual and
+ * converged flag */
+int32_t jgs2_precompute_export(jgs2_ctx* ctx, int64_t* vertices, double* gbar, int64_t* vrows_ptr,
+                               int64_t* vrows_keys, double* vrows, int64_t* cub_ptr, int64_t* cub_elems,
+                               double* cub_weights, double* residual, uint8_t* converged);
+
 /* ---- symbolic analysis (host only; no device needed) ------------------ */
 typedef struct jgs2_sym jgs2_sym;
 jgs2_sym* jgs2_sym_build(int64_t n, const int64_t* adj_ptr, const int32_t* adj,

@@ -27,6 +27,8 @@ EXPORTS = (
     "jgs2_set_frame_state", "jgs2_frame_begin", "jgs2_frame_end", "jgs2_get_frame_state",
     "jgs2_frame_reset", "jgs2_timestep_host", "jgs2_nccl_unique_id", "jgs2_set_comm_nccl",
     "jgs2_set_comm_nccl_handle", "jgs2_set_comm_host", "jgs2_set_partition", "jgs2_create_on_stream",
+    "jgs2_selected_inverse", "jgs2_inverse_blocks", "jgs2_stencil_gradients", "jgs2_precompute_train",
+    "jgs2_precompute_export",
 )
 PHASES = ("vertex_pass", "collect_rhs", "factor_solve", "cubature_hessians", "local_systems",
           "energy", "update", "contact_pairs", "contact_cap", "contact_trials", "frame_cap")
@@ -78,6 +80,12 @@ class SweepInfo(C.Structure):
     _fields_ = [("line_search_activations", i64), ("max_local_step", f64), ("grad_norm", f64),
                 ("grad_sq", f64), ("dx_norm", f64), ("energy", f64), ("halvings", i32),
                 ("n_pairs", i32), ("n_indefinite", i32), ("pad_", i32), ("gamma", f64), ("cap", f64)]
+
+
+class TrainParams(C.Structure):
+    _fields_ = [("n_poses", i32), ("candidates_per_round", i32), ("max_size", i32), ("pad_", i32),
+                ("target_residual", f64), ("seed", C.c_uint64), ("pose_grads", P(f64)),
+                ("pose_solves", P(f64))]
 
 
 class FactorInfo(C.Structure):
@@ -150,6 +158,12 @@ def lib():
         "jgs2_set_comm_host": (i32, [vp, i32, i32, vp, vp]),
         "jgs2_set_partition": (i32, [vp, i64, i64]),
         "jgs2_create_on_stream": (vp, [i32, vp]),
+        "jgs2_selected_inverse": (i32, [vp, P(f64)]),
+        "jgs2_inverse_blocks": (i32, [vp, i64, P(i64), P(i64), P(f64), P(i32)]),
+        "jgs2_stencil_gradients": (i32, [vp, P(f64), P(f64), f64, P(f64)]),
+        "jgs2_precompute_train": (i32, [vp, P(TrainParams), P(i64)]),
+        "jgs2_precompute_export": (i32, [vp, P(i64), P(f64), P(i64), P(i64), P(f64), P(i64), P(i64), P(f64),
+                                         P(f64), P(u8)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

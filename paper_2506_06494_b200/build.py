@@ -66,10 +66,10 @@ def build(force=False, verbose=False):
     tmp = LIB.with_suffix(f".so.tmp{os.getpid()}")
     ninc, nlib = nccl_dirs()
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xptxas", "-O3", "-I", str(PKG.parent / "include"), "-I", str(ninc),
+           "-Xptxas", "-O3", "-Xcompiler", "-fopenmp", "-I", str(PKG.parent / "include"), "-I", str(ninc),
            *[str(CSRC / s) for s in SOURCES], "-o", str(tmp),
            "-L", str(libdir), f"-Xlinker=-rpath,{libdir}", "-lcusolver", "-lcublas",
-           "-L", str(nlib), f"-Xlinker=-rpath,{nlib}", "-l:libnccl.so.2"]
+           "-L", str(nlib), f"-Xlinker=-rpath,{nlib}", "-l:libnccl.so.2", "-lgomp"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))

@@ -5,6 +5,7 @@
 #include <cusolverDn.h>
 
 #include <cstdint>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -117,6 +118,15 @@ struct Factor {
   int* gat_src = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   int64_t graph_launches = 0;
+  // host copies of the front metadata (selected inversion, selinv.cuh)
+  std::vector<int> h_ns, h_nr, h_fld, h_pfront, h_pos;
+  std::vector<int64_t> h_loff, h_sptr;
+  double* Z = nullptr;         // selected inverse, layout of L (after jgs2_selected_inverse)
+  int* d_pfront = nullptr;
+  int* d_cbeg = nullptr;
+  int* d_cend = nullptr;
+  int64_t* d_spptr = nullptr;
+  int* d_spos = nullptr;
   double* u = nullptr;         // update vectors
   double* w = nullptr;         // work vectors (global fallback)
   int max_nf = 0;
@@ -331,6 +341,7 @@ struct Ctx {
   }
 
   Factor fac;
+  std::shared_ptr<struct TrainOut> train;  // scalable precompute output (train.cuh)
   cublasHandle_t cublas = nullptr;
   cusolverDnHandle_t cusolver = nullptr;
 

@@ -577,6 +577,9 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
   std::vector<int> pos(nv, -1), freel(n);
   for (int i = 0; i < n; ++i) { pos[glob[i]] = S.iperm[i]; freel[i] = glob[i]; }
   C.pos = C.upload(pos.data(), nv);
+  F.h_ns = fns; F.h_nr = fnr; F.h_fld = fld; F.h_pos = pos;
+  F.h_loff.assign(loff.begin(), loff.end());
+  F.h_sptr.assign(sptr.begin(), sptr.end());
 
   // ---- Hbar blocks (projected rest element Hessians, subspace.py:48-57)
   double* mp_all = nullptr;

@@ -16,6 +16,8 @@
 #include "hier_grid.cuh"
 #include "partition.cuh"
 #include "comm.cuh"
+#include "selinv.cuh"
+#include "train.cuh"
 
 using namespace jgs2;
 
@@ -739,7 +741,7 @@ int32_t jgs2_set_partition(jgs2_ctx* ctx, int64_t v_begin, int64_t v_end) {
     for (int v = C.own_v0; v < C.own_v1; ++v)
       if (!C.h_fixed[v]) freel.push_back(v);
     C.nfree = (int)freel.size();
-    C.free_list = C.upload(freel.data(), std::max<size_t>(freel.size(), 1));
+    C.free_list = C.upload(freel.data(), freel.size());
     C.partitioned = C.own_v0 != 0 || C.own_v1 != C.nv || (C.comm && C.comm->world > 1);
     // rotations of other ranks' vertices stay zero (jgs2_get_rotations sums)
     JGS2_CUDA(cudaMemsetAsync(C.R, 0, 9 * (size_t)C.nv * sizeof(double), C.stream));
@@ -1422,6 +1424,87 @@ int32_t jgs2_local_step(jgs2_ctx* ctx, double* delta, double* alpha, int64_t* ac
     JGS2_CUDA(cudaFreeAsync(dal, C.stream));
     C.sync();
     if (activations) *activations = C.local_line_search ? lsf[2] : 0;
+  });
+}
+
+// ---- scalable precompute (selinv.cuh, train.cuh)
+int32_t jgs2_selected_inverse(jgs2_ctx* ctx, double* seconds) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (!C.fac.ready) throw Error(JGS2_E_ARG, "rest factor not built");
+    auto t0 = std::chrono::steady_clock::now();
+    selected_inverse(C);
+    if (seconds) *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+int32_t jgs2_inverse_blocks(jgs2_ctx* ctx, int64_t n, const int64_t* v, const int64_t* w, double* out,
+                            int32_t* found) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (!C.fac.Z) throw Error(JGS2_E_ARG, "selected inverse not computed");
+    if (n <= 0) return;
+    int64_t *dv = nullptr, *dw = nullptr;
+    double* dout = nullptr;
+    int* dfound = nullptr;
+    JGS2_CUDA(cudaMallocAsync(&dv, n * sizeof(int64_t), C.stream));
+    JGS2_CUDA(cudaMallocAsync(&dw, n * sizeof(int64_t), C.stream));
+    JGS2_CUDA(cudaMallocAsync(&dout, 9 * n * sizeof(double), C.stream));
+    JGS2_CUDA(cudaMallocAsync(&dfound, n * sizeof(int), C.stream));
+    JGS2_CUDA(cudaMemcpyAsync(dv, v, n * sizeof(int64_t), cudaMemcpyHostToDevice, C.stream));
+    JGS2_CUDA(cudaMemcpyAsync(dw, w, n * sizeof(int64_t), cudaMemcpyHostToDevice, C.stream));
+    k_inverse_blocks<<<grid_for(n), kBlock, 0, C.stream>>>(selinv_dev(C), (int)n, dv, dw, dout, dfound);
+    C.check_launch();
+    JGS2_CUDA(cudaMemcpyAsync(out, dout, 9 * n * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    JGS2_CUDA(cudaMemcpyAsync(found, dfound, n * sizeof(int), cudaMemcpyDeviceToHost, C.stream));
+    for (void* p : {(void*)dv, (void*)dw, (void*)dout, (void*)dfound}) JGS2_CUDA(cudaFreeAsync(p, C.stream));
+    C.sync();
+  });
+}
+
+int32_t jgs2_stencil_gradients(jgs2_ctx* ctx, const double* x, const double* z, double h, double* out) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (!C.have_model) throw Error(JGS2_E_ARG, "model not set");
+    size_t n = 3 * (size_t)C.nv;
+    double *dx = nullptr, *dz = nullptr, *dout = nullptr;
+    JGS2_CUDA(cudaMallocAsync(&dx, n * sizeof(double), C.stream));
+    JGS2_CUDA(cudaMallocAsync(&dz, n * sizeof(double), C.stream));
+    JGS2_CUDA(cudaMallocAsync(&dout, 12 * (size_t)C.ne * sizeof(double), C.stream));
+    JGS2_CUDA(cudaMemcpyAsync(dx, x, n * sizeof(double), cudaMemcpyHostToDevice, C.stream));
+    JGS2_CUDA(cudaMemcpyAsync(dz, z, n * sizeof(double), cudaMemcpyHostToDevice, C.stream));
+    k_stencil_grads<<<grid_for(C.ne), kBlock, 0, C.stream>>>(devmodel(C), dx, dz, h, dout);
+    C.check_launch();
+    JGS2_CUDA(cudaMemcpyAsync(out, dout, 12 * (size_t)C.ne * sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+    for (void* p : {(void*)dx, (void*)dz, (void*)dout}) JGS2_CUDA(cudaFreeAsync(p, C.stream));
+    C.sync();
+  });
+}
+
+int32_t jgs2_precompute_train(jgs2_ctx* ctx, const jgs2_train_params* p, int64_t* sizes) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (!C.fac.Z) throw Error(JGS2_E_ARG, "selected inverse not computed");
+    if (!p || p->n_poses < 0 || (p->n_poses > 0 && (!p->pose_grads || !p->pose_solves)))
+      throw Error(JGS2_E_ARG, "invalid training inputs");
+    TrainParams P{p->n_poses, p->candidates_per_round, p->max_size, p->target_residual, p->seed,
+                  p->pose_grads, p->pose_solves};
+    C.train = std::make_shared<TrainOut>();
+    train_all_host(C, P, *C.train);
+    if (sizes) {
+      sizes[0] = (int64_t)C.train->vertices.size();
+      sizes[1] = (int64_t)C.train->vr_keys.size();
+      sizes[2] = (int64_t)C.train->cub_elems.size();
+    }
+  });
+}
+
+int32_t jgs2_precompute_export(jgs2_ctx* ctx, int64_t* vertices, double* gbar, int64_t* vrows_ptr,
+                               int64_t* vrows_keys, double* vrows, int64_t* cub_ptr, int64_t* cub_elems,
+                               double* cub_weights, double* residual, uint8_t* converged) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (!C.train) throw Error(JGS2_E_ARG, "jgs2_precompute_train first");
+    const TrainOut& T = *C.train;
+    auto cp = [](auto* dst, const auto& v) { if (dst && !v.empty()) memcpy(dst, v.data(), v.size() * sizeof(v[0])); };
+    cp(vertices, T.vertices); cp(gbar, T.gbar); cp(vrows_ptr, T.vr_ptr); cp(vrows_keys, T.vr_keys);
+    cp(vrows, T.vrows); cp(cub_ptr, T.cub_ptr); cp(cub_elems, T.cub_elems); cp(cub_weights, T.cub_w);
+    cp(residual, T.residual); cp(converged, T.converged);
   });
 }
 

@@ -94,6 +94,41 @@ k_vertex_pass(DevModel m, const double* __restrict__ x, const double* __restrict
   }
 }
 
+// Element stencil gradients (cubature.stencil_gradients, cubature.py:37-60):
+// V P W^T per corner plus the element's quarter-mass inertia share,
+// out[12 e + 3 a + r] (vertex-major element DOFs).
+__global__ void __launch_bounds__(kBlock)
+k_stencil_grads(DevModel m, const double* __restrict__ x, const double* __restrict__ z, double h, double* out) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m.ne) return;
+  int4 t = __ldg(m.tets + e);
+  int cs[4] = {t.x, t.y, t.z, t.w};
+  double D[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) D[i] = __ldg(m.dminv + 9 * (size_t)e + i);
+  double xa[4][3];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) xa[a][c] = x[3 * cs[a] + c];
+  double F[9], P[9];
+  deformation_gradient(xa[0], xa[1], xa[2], xa[3], D, F);
+  double4 ep = m.eprops[e];
+  snh_piola(F, snh_const(ep.y, ep.z), P);
+  double h2 = h * h;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    double Wm[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) Wm[j] = a == 0 ? -(D[j] + D[3 + j] + D[6 + j]) : D[3 * (a - 1) + j];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      double s = Wm[0] * P[3 * r] + Wm[1] * P[3 * r + 1] + Wm[2] * P[3 * r + 2];
+      out[12 * (size_t)e + 3 * a + r] = ep.x * s + ep.w * ((xa[a][r] - z[3 * cs[a] + r]) / h2);
+    }
+  }
+}
+
 // y = R^T g into the ND-ordered rhs for free vertices (local_solver.py:124-125);
 // grad_sq is reduced in vertex chunks (partition.cuh)
 __global__ void __launch_bounds__(kBlock)

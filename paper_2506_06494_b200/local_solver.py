@@ -211,44 +211,7 @@ class LocalSolver:
         L.check(fn(self._ctx, *args), self._ctx)
 
     def _upload_model(self, m):
-        k = self._keep
-        arr = lambda a, f: k.append(f(a)) or k[-1]  # noqa: E731
-        nv, ne = int(m.num_vertices), int(np.asarray(m.tets).shape[0])
-        d = L.Model()
-        d.nv, d.ne = nv, ne
-        d.rest_positions = L.ptr(arr(m.rest_positions, L.f64a), L.f64)
-        d.tets = L.ptr(arr(m.tets, L.i64a), L.i64)
-        d.dm_inv = L.ptr(arr(m.dm_inv, L.f64a), L.f64)
-        d.volumes = L.ptr(arr(m.volumes, L.f64a), L.f64)
-        d.mu = L.ptr(arr(m.mu, L.f64a), L.f64)
-        d.lam = L.ptr(arr(m.lam, L.f64a), L.f64)
-        d.elem_qmass = L.ptr(arr(m.elem_qmass, L.f64a), L.f64)
-        d.masses = L.ptr(arr(m.masses, L.f64a), L.f64)
-        d.fixed_mask = L.ptr(arr(np.asarray(m.fixed_mask, dtype=np.uint8), np.ascontiguousarray), L.u8)
-        d.norm_scale = float(m.normalization.scale)
-        bar = getattr(m, "barrier", None)
-        d.has_barrier = 0 if bar is None else 1
-        if bar is not None:
-            d.dhat, d.kappa = float(bar.dhat), float(bar.kappa)
-            planes = list(getattr(m, "planes", []) or [])
-            d.n_planes = len(planes)
-            pts = np.array([p.point for p in planes], dtype=np.float64).reshape(-1, 3)
-            nrm = np.array([p.normal for p in planes], dtype=np.float64).reshape(-1, 3)
-            d.plane_points = L.ptr(arr(pts, L.f64a), L.f64)
-            d.plane_normals = L.ptr(arr(nrm, L.f64a), L.f64)
-            d.n_bodies = len(m.bodies)
-            sv = arr(m.surface_vertices, L.i64a)
-            st = arr(m.surface_tris, L.i64a)
-            d.n_surface_vertices, d.n_surface_tris = sv.size, st.shape[0] if st.ndim == 2 else 0
-            d.surface_vertices = L.ptr(sv, L.i64)
-            d.surface_tris = L.ptr(st, L.i64)
-            d.vertex_body = L.ptr(arr(m.vertex_body, L.i64a), L.i64)
-            d.surface_tri_body = L.ptr(arr(m.surface_tri_body, L.i64a), L.i64)
-        else:
-            d.n_bodies = len(getattr(m, "bodies", [0]))
-            if getattr(m, "vertex_body", None) is not None:
-                d.vertex_body = L.ptr(arr(m.vertex_body, L.i64a), L.i64)
-        self._call(self._lib.jgs2_set_model, C_ref(d))
+        upload_model(self._lib, self._ctx, m, self._keep)
 
     def _upload_precompute(self, p, cfg):
         k = self._keep
@@ -563,6 +526,49 @@ class LocalSolver:
                 cap = int(cnt.value)
                 continue
             L.check(code, self._ctx)
+
+
+def upload_model(lib, ctx, m, keep):
+    """jgs2_set_model from a reference-style Model (assembly.py:40-116); host
+    arrays are kept alive in ``keep`` until the call returns."""
+    k = keep
+    arr = lambda a, f: k.append(f(a)) or k[-1]  # noqa: E731
+    nv, ne = int(m.num_vertices), int(np.asarray(m.tets).shape[0])
+    d = L.Model()
+    d.nv, d.ne = nv, ne
+    d.rest_positions = L.ptr(arr(m.rest_positions, L.f64a), L.f64)
+    d.tets = L.ptr(arr(m.tets, L.i64a), L.i64)
+    d.dm_inv = L.ptr(arr(m.dm_inv, L.f64a), L.f64)
+    d.volumes = L.ptr(arr(m.volumes, L.f64a), L.f64)
+    d.mu = L.ptr(arr(m.mu, L.f64a), L.f64)
+    d.lam = L.ptr(arr(m.lam, L.f64a), L.f64)
+    d.elem_qmass = L.ptr(arr(m.elem_qmass, L.f64a), L.f64)
+    d.masses = L.ptr(arr(m.masses, L.f64a), L.f64)
+    d.fixed_mask = L.ptr(arr(np.asarray(m.fixed_mask, dtype=np.uint8), np.ascontiguousarray), L.u8)
+    d.norm_scale = float(m.normalization.scale)
+    bar = getattr(m, "barrier", None)
+    d.has_barrier = 0 if bar is None else 1
+    if bar is not None:
+        d.dhat, d.kappa = float(bar.dhat), float(bar.kappa)
+        planes = list(getattr(m, "planes", []) or [])
+        d.n_planes = len(planes)
+        pts = np.array([p.point for p in planes], dtype=np.float64).reshape(-1, 3)
+        nrm = np.array([p.normal for p in planes], dtype=np.float64).reshape(-1, 3)
+        d.plane_points = L.ptr(arr(pts, L.f64a), L.f64)
+        d.plane_normals = L.ptr(arr(nrm, L.f64a), L.f64)
+        d.n_bodies = len(m.bodies)
+        sv = arr(m.surface_vertices, L.i64a)
+        st = arr(m.surface_tris, L.i64a)
+        d.n_surface_vertices, d.n_surface_tris = sv.size, st.shape[0] if st.ndim == 2 else 0
+        d.surface_vertices = L.ptr(sv, L.i64)
+        d.surface_tris = L.ptr(st, L.i64)
+        d.vertex_body = L.ptr(arr(m.vertex_body, L.i64a), L.i64)
+        d.surface_tri_body = L.ptr(arr(m.surface_tri_body, L.i64a), L.i64)
+    else:
+        d.n_bodies = len(getattr(m, "bodies", [0]))
+        if getattr(m, "vertex_body", None) is not None:
+            d.vertex_body = L.ptr(arr(m.vertex_body, L.i64a), L.i64)
+    L.check(lib.jgs2_set_model(ctx, C_ref(d)), ctx)
 
 
 def C_ref(obj):
