@@ -232,6 +232,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--frames", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-precompute", action="store_true")
+    ap.add_argument("--precompute-sweeps", type=int, default=30)
     args = ap.parse_args()
     from paper_2506_06494_b200 import replicas
     world, rank, local, dist = replicas.setup()
@@ -360,6 +362,17 @@ def main():
     e2e = (e2e_sweeps / replicas.max_over_ranks(dist, e2e_s) if partitioned
            else replicas.job_throughput(dist, e2e_sweeps, e2e_s))
 
+    # the scalable precompute at this config, and sweeps driven
+    # by it: the reference algorithm's own bases/cubature instead of the
+    # injected ones (rank 0 only, after the timed windows)
+    scal = None
+    if rank == 0 and not args.no_precompute:
+        solver.close()
+        try:
+            scal = scalable_block(m, h, cfg, init, args.precompute_sweeps)
+        except Exception as exc:  # never fail the GPU line on this block
+            scal = {"failed": str(exc)}
+
     cpu, compare = None, None
     if rank == 0 and not args.no_cpu:
         try:
@@ -414,10 +427,38 @@ def main():
         "clocks": clk,
         "cpu_baseline": cpu,
         "cpu_vs_gpu_same_config": compare,
+        "precompute_scalable": scal,
     }
     print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()
+
+
+def scalable_block(m, h, cfg, init, sweeps):
+    """Device precompute of the scene (precompute_gpu.py) and ``sweeps``
+    sweeps of the continuing simulation driven by it."""
+    from paper_2506_06494_b200.local_solver import LocalSolver
+    from paper_2506_06494_b200.precompute_gpu import scalable_precompute
+    t0 = time.perf_counter()
+    pre, info = scalable_precompute(m, h)
+    out = {"seconds": round(time.perf_counter() - t0, 2)}
+    res = info.pop("residual")
+    info.pop("converged")
+    out.update({k: (round(v, 4) if isinstance(v, float) else v) for k, v in info.items()})
+    out["residual_p90"] = float(np.quantile(res, 0.9)) if res.size else 0.0
+    s = LocalSolver(m, cfg, precompute=pre, h_ref=h)
+    s.set_frame_state(init, m.gravity)
+    s.run_sweeps(2)
+    rec = []
+    s.timer_start()
+    frames = s.run_sweeps(sweeps, rec)
+    ms = s.timer_stop()
+    hv = np.array([r["halvings"] for r in rec])
+    out.update({"sweeps_s": sweeps / (ms / 1e3), "sweeps": sweeps, "frames_completed": frames,
+                "halvings_hist": {str(k): int(c) for k, c in zip(*np.unique(hv, return_counts=True))},
+                "frac_le5_halvings": float(np.mean(hv <= 5)), "floored": int(np.sum(hv > cfg.max_halvings))})
+    s.close()
+    return out
 
 
 def host_info():

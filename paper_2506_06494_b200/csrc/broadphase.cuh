@@ -12,6 +12,8 @@
 // cell stay in ascending id order): candidates arrive in the reference's
 // row-major (vertex, triangle) order without a per-vertex sort.
 #pragma once
+#include <chrono>
+#include <cstdio>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -155,16 +157,22 @@ inline void tri_grid_build(Ctx& C, TriGrid& g, const double* x, const double* dx
   C.check_launch();
   size_t tb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tb, g.counts, g.off, nst + 1, C.stream);
-  if (tb > g.temp_bytes) {
+  if (tb > g.temp_bytes) {  // grow with slack: cudaFree/cudaMalloc stall the device
     cudaFree(g.temp);
-    JGS2_CUDA(cudaMalloc(&g.temp, tb));
-    g.temp_bytes = tb;
+    JGS2_CUDA(cudaMalloc(&g.temp, 2 * tb));
+    g.temp_bytes = 2 * tb;
   }
   JGS2_CUDA(cub::DeviceScan::ExclusiveSum(g.temp, tb, g.counts, g.off, nst + 1, C.stream));
   ++C.launches;
   long long total = 0;
+  static const bool dbg = getenv("JGS2_DEBUG_PAIRS") != nullptr;
+  auto tq = std::chrono::steady_clock::now();
   JGS2_CUDA(cudaMemcpyAsync(&total, g.off + nst, sizeof(long long), cudaMemcpyDeviceToHost, C.stream));
   C.sync();
+  if (dbg) {
+    double w = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tq).count();
+    if (w > 20.0) fprintf(stderr, "grid: count+scan sync waited %.2f ms\n", w);
+  }
   if (total < 0 || total > 64LL * (nst + 1) + (1LL << 24))
     throw Error(-2, "broadphase: grid entry count " + std::to_string(total) +
                         " out of range (non-finite positions or oversized query radius)");
@@ -184,14 +192,20 @@ inline void tri_grid_build(Ctx& C, TriGrid& g, const double* x, const double* dx
   size_t sb = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, sb, g.keys_a, g.keys_b, g.tris_a, g.tris_b, (int)total, 0, 63,
                                   C.stream);
-  if (sb > g.temp_bytes) {
+  if (sb > g.temp_bytes) {  // the sort's scratch grows with the entry count: 1.5x slack
     cudaFree(g.temp);
-    JGS2_CUDA(cudaMalloc(&g.temp, sb));
-    g.temp_bytes = sb;
+    JGS2_CUDA(cudaMalloc(&g.temp, sb + sb / 2));
+    g.temp_bytes = sb + sb / 2;
   }
   JGS2_CUDA(cub::DeviceRadixSort::SortPairs(g.temp, sb, g.keys_a, g.keys_b, g.tris_a, g.tris_b, (int)total,
                                             0, 63, C.stream));
   ++C.launches;
+  if (dbg) {
+    auto ts = std::chrono::steady_clock::now();
+    C.sync();
+    double w = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ts).count();
+    if (w > 20.0) fprintf(stderr, "grid: write+sort took %.2f ms (entries %lld)\n", w, total);
+  }
 }
 
 }  // namespace jgs2

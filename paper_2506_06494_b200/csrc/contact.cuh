@@ -8,6 +8,8 @@
 // set is bit-exact: 3-term dots as (p0+p2)+p1 without FMA,
 // norms as sqrt((x^2+y^2)+z^2), region tests in the reference's order.
 #pragma once
+#include <chrono>
+#include <cstdio>
 #include "context.cuh"
 #include "sweep.cuh"
 #include "geometry.cuh"
@@ -571,8 +573,8 @@ void scan_ints(Ctx& C, int* in, int* out, int n) {
   size_t tb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n + 1, C.stream);
   if (tb > C.scan_temp_bytes) {
-    C.scan_temp = C.alloc<char>(tb);
-    C.scan_temp_bytes = tb;
+    C.scan_temp = C.alloc<char>(tb + tb / 2);
+    C.scan_temp_bytes = tb + tb / 2;
   }
   JGS2_CUDA(cub::DeviceScan::ExclusiveSum(C.scan_temp, tb, in, out, n + 1, C.stream));
   ++C.launches;
@@ -588,23 +590,33 @@ void contact_find_pairs(Ctx& C, const double* x, const double* dx, double gamma)
   JGS2_CUDA(cudaMemsetAsync(C.flag_d, 0, sizeof(int), C.stream));
   int ug = use_tri_grid(C) ? 1 : 0;
   TriGridDev gd{nullptr, nullptr, 0, 1.0};
+  static const bool dbg = getenv("JGS2_DEBUG_PAIRS") != nullptr;
+  using clk = std::chrono::steady_clock;
+  auto ms = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+  auto t0 = clk::now();
   if (ug) {
     tri_grid_build(C, C.pair_grid, x, dx, gamma, C.dhat * (1.0 + 1e-6) + 1e-300, C.grid_cell);
     gd = grid_dev(C.pair_grid);
   } else {
     cd.nst = 0;  // single body: no cross-body triangle pairs
   }
+  auto t1 = clk::now();
   k_pair_count<<<grid_for(C.nsv, 128), 128, 0, C.stream>>>(cd, gd, ug, x, dx, gamma, C.pair_count_sv);
   C.check_launch();
   scan_ints(C, C.pair_count_sv, C.pair_off_sv, n);
   int total = 0;
   JGS2_CUDA(cudaMemcpyAsync(&total, C.pair_off_sv + n, sizeof(int), cudaMemcpyDeviceToHost, C.stream));
   C.sync();
+  auto t2 = clk::now();
   ensure_pair_capacity(C, total);
+  auto t3 = clk::now();
   k_pair_write<<<grid_for(C.nsv, 128), 128, 0, C.stream>>>(cd, gd, ug, x, dx, gamma, C.pair_off_sv,
                                                            (int)C.cap_pairs, C.pairs, C.flag_d);
   C.check_launch();
   C.npairs = total;
+  if (dbg && ms(t0, t3) > 20.0)
+    fprintf(stderr, "find_pairs slow: grid %.2f ms (entries %lld) count+scan+sync %.2f ms alloc %.2f ms pairs %d\n",
+            ms(t0, t1), C.pair_grid.n, ms(t1, t2), ms(t2, t3), total);
 }
 
 bool contact_infeasible(Ctx& C) {

@@ -561,7 +561,7 @@ inline long long scan_counts(Ctx& C, long long* cnt, long long* off, long long n
   JGS2_CUDA(cudaMemsetAsync(cnt + n, 0, sizeof(long long), C.stream));
   size_t tb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, n + 1, C.stream);
-  if (tb > C.scan_temp_bytes) { C.scan_temp = C.alloc<char>(tb); C.scan_temp_bytes = tb; }
+  if (tb > C.scan_temp_bytes) { C.scan_temp = C.alloc<char>(tb + tb / 2); C.scan_temp_bytes = tb + tb / 2; }
   JGS2_CUDA(cub::DeviceScan::ExclusiveSum(C.scan_temp, tb, cnt, off, n + 1, C.stream));
   ++C.launches;
   long long total = 0;
@@ -616,7 +616,7 @@ inline void hier_prepare(Ctx& C, HierArgs& a, const double* bb) {
   while (bits < 32 && (1ull << bits) < (unsigned long long)ndir) ++bits;
   size_t sb = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, sb, h.ka, h.kb, h.ia, h.ib, (int)total, 0, bits, C.stream);
-  if (sb > C.scan_temp_bytes) { C.scan_temp = C.alloc<char>(sb); C.scan_temp_bytes = sb; }
+  if (sb > C.scan_temp_bytes) { C.scan_temp = C.alloc<char>(sb + sb / 2); C.scan_temp_bytes = sb + sb / 2; }
   JGS2_CUDA(cub::DeviceRadixSort::SortPairs(C.scan_temp, sb, h.ka, h.kb, h.ia, h.ib, (int)total, 0, bits,
                                             C.stream));
   ++C.launches;
@@ -625,7 +625,7 @@ inline void hier_prepare(Ctx& C, HierArgs& a, const double* bb) {
   C.check_launch();
   size_t tb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tb, h.flag, h.rix, (int)total, C.stream);
-  if (tb > C.scan_temp_bytes) { C.scan_temp = C.alloc<char>(tb); C.scan_temp_bytes = tb; }
+  if (tb > C.scan_temp_bytes) { C.scan_temp = C.alloc<char>(tb + tb / 2); C.scan_temp_bytes = tb + tb / 2; }
   JGS2_CUDA(cub::DeviceScan::ExclusiveSum(C.scan_temp, tb, h.flag, h.rix, (int)total, C.stream));
   ++C.launches;
   k_hier_runs<<<grid_for(total), kBlock, 0, C.stream>>>(cd, h.kb, h.ib, total, a.g.ncells, h.flag, h.rix,
