@@ -229,7 +229,7 @@ def main():
     # C4 (3.5M tets, ten puffer balls, IPC) is the configuration BASELINE.json's
     # metric is quoted on; C3 (1M-tet twist, no contact) is the elastic-only case
     ap.add_argument("--config", default=os.environ.get("JGS2_BENCH_CONFIG", "c4"))
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--frames", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-precompute", action="store_true")
@@ -342,16 +342,17 @@ def main():
     # LocalSolver.timestep call per frame (jgs2_timestep_host: the frame
     # state x_prev, v goes h2d from pinned host memory, compute_z + capped
     # initialize_step + outer_solve to tol_dx + velocity update run on the
-    # device, the new x_prev, v come back d2h), continuing the simulation
-    import ctypes
+    # device, the new x_prev, v come back d2h), from the scene's initial
+    # state over whole frames covering at least the timed window's sweeps
+    # (the same frames the device-resident window ran)
     nv = m.num_vertices
     xpw, o7 = L.pinned_array((nv, 3))
     vvw, o8 = L.pinned_array((nv, 3))
-    xs, vs = solver.get_frame_state()
-    xpw[:], vvw[:] = xs, vs
+    xpw[:], vvw[:] = init.x_prev, init.v
     e2e_sweeps, e2e_frames, h2d, d2h = 0, 0, 0, 0
     t_e2e = time.perf_counter()
-    while e2e_sweeps < args.e2e_steps:
+    e2e_target = args.e2e_steps if args.e2e_steps is not None else args.warmup + args.steps
+    while e2e_sweeps < e2e_target:
         fs = SystemState(x=None, x_prev=xpw, v=vvw, z=None, h=h)
         it, _ = solver.timestep(fs, m.gravity, x_prev_out=xpw, v_out=vvw)
         h2d += 2 * xpw.nbytes
