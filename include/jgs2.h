@@ -84,7 +84,9 @@ typedef struct jgs2_config {
   int32_t max_halvings;
   double alpha_floor;
   int32_t mode;            /* 0 jacobi, 1 gauss_seidel (local_solver.py:627-649) */
-  int32_t pad_;
+  int32_t subspace;        /* 0 corotated_cubature, 1 none (plain vertex block descent,
+                              local_solver.py:325-353, 472-522; jgs2_set_precompute then
+                              takes pre = NULL and no factor is needed) */
 } jgs2_config;
 
 /* sweep() info dict (local_solver.py:613-614, 654) + extras. */

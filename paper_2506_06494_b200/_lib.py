@@ -73,7 +73,7 @@ class Precompute(C.Structure):
 class Config(C.Structure):
     _fields_ = [("tol_dx", f64), ("max_outer", i32), ("local_line_search", i32),
                 ("track_energy", i32), ("max_halvings", i32), ("alpha_floor", f64),
-                ("mode", i32), ("pad_", i32)]
+                ("mode", i32), ("subspace", i32)]
 
 
 class SweepInfo(C.Structure):

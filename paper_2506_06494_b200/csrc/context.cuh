@@ -150,6 +150,9 @@ struct Ctx {
   bool local_line_search = true, track_energy = true;
   int last_halvings = 0;  // previous sweep's backtracking halvings (sizes the first trial batch)
   int mode = 0;                // 0 jacobi, 1 gauss_seidel
+  bool plain = false;          // subspace="none" (plain.cuh): no precompute, no factor
+  double* mplus_all = nullptr; // plain mode: projected reduced Hessian of every element (45 each)
+  int* hess_list_all = nullptr;
   // Gauss-Seidel colour groups: free vertices by colour (ascending id)
   std::vector<int> color_ptr;
   int* color_verts = nullptr;

@@ -18,6 +18,7 @@
 #include "comm.cuh"
 #include "selinv.cuh"
 #include "train.cuh"
+#include "plain.cuh"
 
 using namespace jgs2;
 
@@ -79,7 +80,7 @@ DevModel devmodel(const Ctx& C) {
 LocalArgs localargs(Ctx& C) {
   LocalArgs a;
   memset(&a, 0, sizeof(a));
-  a.R = C.R; a.b = C.q; a.gbar = C.gbar; a.group = C.group; a.grows = C.grows;
+  a.R = C.R; a.gasm = C.gasm; a.b = C.q; a.gbar = C.gbar; a.group = C.group; a.grows = C.grows;
   a.cub_u = C.cub_u; a.cub_w = C.cub_w; a.cub_rows = C.cub_rows; a.cub_verts = C.cub_verts;
   a.crest = C.crest; a.mplus = C.mplus; a.h = C.h;
   a.delta = C.delta; a.alpha0 = C.alpha0; a.kacc = C.kacc;
@@ -93,7 +94,7 @@ LocalArgs localargs(Ctx& C) {
 void require_ready(Ctx& C) {
   if (!C.have_model) throw Error(JGS2_E_ARG, "model not set");
   if (!C.have_pre) throw Error(JGS2_E_ARG, "precompute not set");
-  if (!C.fac.ready) throw Error(JGS2_E_ARG, "rest factor not built (jgs2_factor_rest)");
+  if (!C.plain && !C.fac.ready) throw Error(JGS2_E_ARG, "rest factor not built (jgs2_factor_rest)");
 }
 
 // ---- algorithmic bytes per phase: unique bytes a
@@ -155,6 +156,10 @@ void gradsq_chunks(Ctx& C) {
 }
 
 void collect(Ctx& C) {
+  if (C.plain) {  // no reduced collect in plain mode (local_solver.py:597): grad_sq only
+    gradsq_chunks(C);
+    return;
+  }
   DevModel m = devmodel(C);
   C.phase_begin(1, bytes_rhs(C));
   k_rhs<<<grid_for(C.nfree), kBlock, 0, C.stream>>>(m, C.R, C.gasm, C.b);
@@ -220,7 +225,19 @@ void local_systems(Ctx& C, double* A_out, double* g_out, double* corr_out, const
   a.x = C.x; a.pairs = C.pairs; a.pair_g = C.pair_g; a.pair_h = C.pair_h;
   a.vp_ptr = C.vp_ptr; a.vp_list = C.vp_list; a.planes = C.planes;
   a.vr_ptr = C.vr_ptr; a.vr_keys = C.vr_keys; a.vr_rows = C.vr_rows;
-  if (m.nfree > 0) k_local<<<grid_for(m.nfree, 128), 128, 0, C.stream>>>(m, a);
+  if (C.plain) {  // own-stencil systems: projected Hessians of every element at the current x
+    C.phase_end();
+    C.phase_begin(3, C.ne * 580.0);
+    launch_element_mplus(C.ne, nullptr, C.x, C.tets, C.dminv, C.eprops, C.mplus_all, C.hess_count,
+                         C.hess_list_all, C.stream);
+    C.launches += 3;
+    C.phase_end();
+    C.phase_begin(4, 0.0);
+    PlainArgs pa{C.mplus_all, C.z, C.dhat, C.kappa};
+    if (m.nfree > 0) k_plain_local<<<grid_for(m.nfree, 128), 128, 0, C.stream>>>(m, a, pa);
+  } else if (m.nfree > 0) {
+    k_local<<<grid_for(m.nfree, 128), 128, 0, C.stream>>>(m, a);
+  }
   C.check_launch();
   // the local search's halving rounds are global (local_solver.py:539-553):
   // counts of unaccepted vertices and the max alpha0 among them per round
@@ -424,7 +441,7 @@ double gauss_seidel_colours(Ctx& C, int* acts, bool hess_ready) {
 // otherwise use the context's current rotations.
 void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
   require_ready(C);
-  if (!rot && !C.rot_valid) throw Error(JGS2_E_ARG, "rotations not set");
+  if (!rot && !C.rot_valid && !C.plain) throw Error(JGS2_E_ARG, "rotations not set");
   DevModel m = devmodel(C);
   bool guard = C.local_line_search;
   // Optional (JGS2_HESS_EARLY=1): element Hessians at x (compute-bound FP64,
@@ -872,7 +889,7 @@ int32_t jgs2_set_model(jgs2_ctx* ctx, const jgs2_model* md) {
 int32_t jgs2_set_precompute(jgs2_ctx* ctx, const jgs2_precompute* p, const jgs2_config* cfg) {
   return guarded(ctx, [&](Ctx& C) {
     if (!C.have_model) throw Error(JGS2_E_ARG, "set the model first");
-    if (!p || !cfg) throw Error(JGS2_E_ARG, "null precompute/config");
+    if (!cfg) throw Error(JGS2_E_ARG, "null config");
     if (C.have_pre) throw Error(JGS2_E_ARG, "precompute already set");
     C.tol_dx = cfg->tol_dx;
     C.max_outer = cfg->max_outer;
@@ -886,6 +903,30 @@ int32_t jgs2_set_precompute(jgs2_ctx* ctx, const jgs2_precompute* p, const jgs2_
     if (C.tol_dx <= 0 || C.max_outer < 1 || C.max_halvings < 0)
       throw Error(JGS2_E_ARG, "invalid solver config");
     const int nv = C.nv;
+    if (cfg->subspace != 0 && cfg->subspace != 1) throw Error(JGS2_E_ARG, "subspace must be 0 or 1");
+    if (cfg->subspace == 1) {  // plain vertex block descent: no bases, no factor
+      C.plain = true;
+      C.smax = 0;
+      if (!C.pos) {  // no factor: free-vertex marker for the update kernels (-1 fixed / other rank)
+        std::vector<int> pos(nv, -1);
+        int k = 0;
+        for (int v = 0; v < nv; ++v)
+          if (!C.h_fixed[v] && C.owns(v)) pos[v] = k++;
+        C.pos = C.upload(pos.data(), nv);
+      }
+      C.nuniq = 0;
+      C.nslots = 0;
+      C.mplus_all = C.alloc<double>(45 * (size_t)std::max(C.ne, 1));
+      C.hess_list_all = C.alloc<int>(2 * (size_t)std::max(C.ne, 1));
+      C.ls_max = C.alloc<unsigned long long>(C.max_halvings + 2);
+      C.ls_cnt = C.alloc<int>(C.max_halvings + 2);
+      C.ls_final = C.alloc<int>(4);
+      JGS2_CUDA(cudaMemsetAsync(C.ls_final, 0, 4 * sizeof(int), C.stream));
+      C.have_pre = true;
+      C.sync();
+      return;
+    }
+    if (!p) throw Error(JGS2_E_ARG, "null precompute");
     const int64_t nb = p->n_bases;
     C.gmax = (int)std::max<int64_t>(p->gmax, 1);
     std::vector<int> bidx(nv, -1);

@@ -152,6 +152,7 @@ __device__ __forceinline__ void q_of(const DevModel& m, const double* b, int w, 
 
 struct LocalArgs {
   const double* R;
+  const double* gasm;       // assembled field (plain mode)
   const double* b;          // collect solution q (ND order)
   const double* gbar;       // nv*9
   const int* group;         // nv*gmax

@@ -156,16 +156,20 @@ class LocalSolver:
                  comm="nccl"):
         self.model = model
         self.config = config
-        if config.subspace != "corotated_cubature":
-            raise ValueError(f"subspace {config.subspace!r} is not on the GPU path "
-                             "(only corotated_cubature; see SURVEY §2.1)")
-        if precompute is None:
+        self.plain = config.subspace == "none"  # plain vertex block descent (local_solver.py:325-353)
+        if config.subspace == "exact":
+            raise ValueError("subspace 'exact' (the <=6000-DOF verification path) is not on the GPU path")
+        if self.plain:
+            precompute = None
+        elif precompute is None:
             if not bases:
                 raise ValueError("corotated_cubature needs precomputed bases")
             precompute = Precompute.from_reference(bases, cubature_sets or {})
-        if hbar is None and factor is not None and hasattr(factor, "perm_r"):
+        if not self.plain and hbar is None and factor is not None and hasattr(factor, "perm_r"):
             hbar = hbar_from_factor(factor, model)
-        if hbar is None and h_ref is None:
+        if self.plain:
+            pass
+        elif hbar is None and h_ref is None:
             if isinstance(factor, (int, float)):
                 h_ref = float(factor)
             elif factor is not None and hasattr(factor, "h_ref"):
@@ -194,7 +198,9 @@ class LocalSolver:
             self._call(self._lib.jgs2_set_partition, int(self.partition[0]), int(self.partition[1]))
         t0 = time.perf_counter()
         self.factor_info = L.FactorInfo()
-        if hbar is not None:
+        if self.plain:
+            pass
+        elif hbar is not None:
             br, bc, bv = matrix_blocks(hbar)
             self._call(self._lib.jgs2_factor_blocks, br.size, L.ptr(br, L.i64), L.ptr(bc, L.i64),
                        L.ptr(bv, L.f64), int(leaf_size), C_ref(self.factor_info))
@@ -216,6 +222,14 @@ class LocalSolver:
     def _upload_precompute(self, p, cfg):
         k = self._keep
         arr = lambda a, f: k.append(f(a)) or k[-1]  # noqa: E731
+        if p is None:  # plain mode: configuration only
+            c = self._config_struct(cfg)
+            c.subspace = 1
+            self._call(self._lib.jgs2_set_precompute, None, C_ref(c))
+            if cfg.mode == "gauss_seidel":
+                colors = L.i64a(self.model.colors)
+                self._call(self._lib.jgs2_set_colors, L.ptr(colors, L.i64))
+            return
         d = L.Precompute()
         d.n_bases = int(np.asarray(p.vertices).size)
         d.gmax = int(np.asarray(p.group).shape[1])
@@ -229,6 +243,14 @@ class LocalSolver:
         d.cub_ptr = L.ptr(arr(p.cub_ptr, L.i64a), L.i64)
         d.cub_elems = L.ptr(arr(p.cub_elems, L.i64a), L.i64)
         d.cub_weights = L.ptr(arr(p.cub_weights, L.f64a), L.f64)
+        c = self._config_struct(cfg)
+        self._call(self._lib.jgs2_set_precompute, C_ref(d), C_ref(c))
+        if cfg.mode == "gauss_seidel":  # colour groups (local_solver.py:298-303)
+            colors = L.i64a(self.model.colors)
+            self._call(self._lib.jgs2_set_colors, L.ptr(colors, L.i64))
+
+    @staticmethod
+    def _config_struct(cfg):
         c = L.Config()
         c.tol_dx = float(cfg.tol_dx)
         c.max_outer = int(cfg.max_outer)
@@ -237,10 +259,8 @@ class LocalSolver:
         c.max_halvings = int(cfg.max_halvings)
         c.alpha_floor = float(cfg.alpha_floor)
         c.mode = SCHEDULES.index(cfg.mode)
-        self._call(self._lib.jgs2_set_precompute, C_ref(d), C_ref(c))
-        if cfg.mode == "gauss_seidel":  # colour groups (local_solver.py:298-303)
-            colors = L.i64a(self.model.colors)
-            self._call(self._lib.jgs2_set_colors, L.ptr(colors, L.i64))
+        c.subspace = 0
+        return c
 
     def close(self):
         if getattr(self, "_ctx", None):
@@ -362,7 +382,7 @@ class LocalSolver:
         self.set_state(state.x, state.z, state.h)
         for _ in range(cfg.max_outer):
             t1 = time.perf_counter()
-            info = self.sweep_resident(refresh_rotations=True)
+            info = self.sweep_resident(refresh_rotations=not self.plain)
             stats.wall_ms.append(1e3 * (time.perf_counter() - t1))
             stats.dx_norms.append(info["dx_norm"])
             stats.grad_norms.append(info["grad_norm"])
@@ -375,7 +395,8 @@ class LocalSolver:
                 stats.converged = True
                 break
         state.x = self.get_x()
-        state.rotations = self.get_rotations()
+        if not self.plain:  # plain mode leaves state.rotations alone (local_solver.py:699-702)
+            state.rotations = self.get_rotations()
         stats.wall_seconds = time.perf_counter() - t0
         return stats
 

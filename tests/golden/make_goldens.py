@@ -185,6 +185,15 @@ def kernel_snapshot(model, solver, state, rot, pairs):
     """Per-kernel intermediates from the reference's private methods."""
     x = state.x.copy()
     verts = solver.free
+    if solver.config.subspace == "none":  # plain VBD (local_solver.py:325-353, 472-522)
+        g_asm = solver._assembled_field(x, state, pairs)
+        a, g = solver._plain_systems(x, state, verts, g_asm, pairs, rot)
+        delta = solver._solve_batch(a, -g)
+        alpha, acts = solver._line_search(x, state, verts, delta, pairs, rot, a, g)
+        e = total_energy(model, state, x, pairs)
+        return {"k_x": x, "k_z": state.z.copy(), "k_rot": np.asarray(rot).copy(), "k_g_asm": g_asm,
+                "k_a": a, "k_g": g, "k_delta": delta, "k_alpha": alpha, "k_acts": np.array([acts]),
+                "k_energy": np.array([e])}
     g_asm = solver._assembled_field(x, state, pairs)
     from tetsolve.local_solver import reduced_collect
     q = reduced_collect(model, solver.factor, rot, g_asm)
@@ -223,7 +232,8 @@ def c1_scene():
 
 # (frame, sweep) of the per-kernel snapshot: a deformed state, in contact
 # for the contact scenes.
-SNAPSHOT = {"cube_drop": (20, 2), "two_body": (25, 2), "cube_drop_gs": (20, 2), "two_body_gs": (25, 2)}
+SNAPSHOT = {"cube_drop": (20, 2), "two_body": (25, 2), "cube_drop_gs": (20, 2), "two_body_gs": (25, 2),
+            "cube_drop_plain": (20, 2), "two_body_plain": (25, 2)}
 
 
 def gauss_seidel(make):
@@ -235,6 +245,17 @@ def gauss_seidel(make):
         return scene, model, frames
     return build
 
+def plain(make):
+    """The same scene with the plain vertex block descent baseline
+    (subspace="none", solver tag plain_local, harness.py:112-113): own-stencil
+    systems, no precompute (local_solver.py:325-353, 472-522)."""
+    def build():
+        scene, model, frames = make()
+        scene.solver.subspace = "none"
+        return scene, model, frames
+    return build
+
+
 SCENES = {
     "beam": lambda: scene_from_toml("beam"),
     "beam_stiff": lambda: scene_from_toml("beam_stiff", frames=3),
@@ -244,6 +265,9 @@ SCENES = {
     "beam_gs": gauss_seidel(lambda: scene_from_toml("beam", frames=3)),
     "cube_drop_gs": gauss_seidel(lambda: scene_from_toml("cube_drop", frames=24)),
     "two_body_gs": gauss_seidel(lambda: scene_from_toml("two_body", frames=28)),
+    "beam_plain": plain(lambda: scene_from_toml("beam", frames=4)),
+    "cube_drop_plain": plain(lambda: scene_from_toml("cube_drop", frames=24)),
+    "two_body_plain": plain(lambda: scene_from_toml("two_body", frames=28)),
 }
 
 
@@ -251,13 +275,16 @@ def main(names):
     for name in names:
         t0 = time.time()
         scene, model, frames = SCENES[name]()
-        runtime = harness.prepare(model, scene, use_cache=False, seed=scene.seed)
+        is_plain = scene.solver.subspace == "none"
+        runtime = (harness.RuntimeData({}, {}, None, None, {}) if is_plain
+                   else harness.prepare(model, scene, use_cache=False, seed=scene.seed))
         t_pre = time.time() - t0
-        solver = harness.make_solver(model, scene, "jgs2_cubature", runtime)
+        solver = harness.make_solver(model, scene, "plain_local" if is_plain else "jgs2_cubature", runtime)
         cfg = solver.config
         data = {}
         data.update(model_arrays(model))
-        data.update(precompute_arrays(runtime.bases, runtime.cubature_sets))
+        if not is_plain:
+            data.update(precompute_arrays(runtime.bases, runtime.cubature_sets))
         data["scene_h"] = np.array([scene.h])
         data["scene_cfg"] = np.array([cfg.tol_dx, cfg.max_outer, cfg.max_halvings,
                                       cfg.alpha_floor, float(cfg.local_line_search),

@@ -10,8 +10,9 @@ POS_RTOL = 1e-9  # north_star: FP64 positions within 1e-9 relative
 
 
 def scene_inputs(g):
+    """(model, precompute or None for plain-mode fixtures, h)."""
     model = Model.from_arrays(g)
-    pre = Precompute.from_arrays(g)
+    pre = Precompute.from_arrays(g) if "pre_vertices" in g else None
     h = float(g["scene_h"][0])
     return model, pre, h
 

@@ -289,3 +289,44 @@ def test_drop_in_reference_objects_match_reference(golden, name):
         stats = s.outer_solve(st)
         assert stats.outer_iterations == int(g["frame_iterations"][f])
         assert rel_err(st.x, g["frame_x_final"][f]) < 1e-9
+
+
+@pytest.mark.parametrize("name", ("beam_plain", "cube_drop_plain", "two_body_plain"))
+def test_plain_vbd_trajectory_matches_reference(golden, name):
+    """subspace="none" (the reference's plain vertex block descent baseline,
+    local_solver.py:325-353, 472-522) against the reference's own plain_local
+    trajectories: pair sets, sweeps per frame, positions."""
+    from paper_2506_06494_b200.model import Model
+    g = golden(name)
+    model = Model.from_arrays(g)
+    h = float(g["scene_h"][0])
+    c = g["scene_cfg"]
+    cfg = SolverConfig(tol_dx=float(c[0]), max_outer=int(c[1]), max_halvings=int(c[2]),
+                       alpha_floor=float(c[3]), local_line_search=bool(c[4]), track_energy=bool(c[5]),
+                       subspace="none")
+    s = LocalSolver(model, cfg)
+
+    def sweep(state):
+        return s.sweep(state)
+
+    rep = replay(g, sweep, s.find_pairs)
+    assert rep["pair_mismatch"] == 0, rep
+    assert rep["iters"] == rep["iters_ref"], rep
+    assert rep["pos"] < 1e-9, rep
+
+
+@pytest.mark.parametrize("name", ("cube_drop_plain", "two_body_plain"))
+def test_plain_vbd_kernels_match_reference(golden, name):
+    from paper_2506_06494_b200.model import Model
+    g = golden(name)
+    model = Model.from_arrays(g)
+    h = float(g["scene_h"][0])
+    s = LocalSolver(model, SolverConfig(subspace="none"))
+    x, z = g["k_x"], g["k_z"]
+    a, gg = s.reduced_systems(x, z, h, g["k_rot"])
+    assert rel_err(a, g["k_a"]) < 1e-10
+    assert rel_err(gg, g["k_g"]) < 1e-10
+    d, al, acts = s.local_step(x, z, h, g["k_rot"])
+    assert rel_err(d, g["k_delta"]) < 1e-10
+    np.testing.assert_allclose(al, g["k_alpha"], rtol=1e-12)
+    assert acts == int(g["k_acts"][0])
