@@ -198,11 +198,14 @@ def cpu_extrapolate(config, budget_s=20.0):
 
 def traffic(config, kernel, launches, steps):
     """DRAM bytes per launch of the roofline kernel from the committed ncu
-    capture (profiles/r1_traffic_<config>.json, dram__bytes_read.sum +
+    capture (profiles/r2_traffic_<config>.json, else r1_; dram__bytes_read.sum +
     dram__bytes_write.sum summed over the kernel's launches in one sweep),
     or None when no capture exists for this config."""
     try:
-        t = json.loads((ROOT / "profiles" / f"r1_traffic_{config}.json").read_text())
+        f = ROOT / "profiles" / f"r2_traffic_{config}.json"
+        if not f.exists():
+            f = ROOT / "profiles" / f"r1_traffic_{config}.json"
+        t = json.loads(f.read_text())
         if t.get("phase") != kernel or not launches:
             return None
         return t["dram_bytes_per_sweep"] / (launches / steps)

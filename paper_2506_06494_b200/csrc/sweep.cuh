@@ -364,14 +364,9 @@ __device__ void sampled_inner(const DevModel& m, const LocalArgs& a, int v, doub
   }
 }
 
-__global__ void __launch_bounds__(128, 4)
-k_local(DevModel m, LocalArgs a) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= m.nfree) return;
-  int v = m.free_list[i];
+// Everything after the sampled sum S of one vertex (local_solver.py:392-553).
+__device__ __forceinline__ void local_tail(const DevModel& m, const LocalArgs& a, int v, const double* S) {
   const double* Ri = a.R + 9 * (size_t)v;
-  double S[9];
-  sampled_inner(m, a, v, S);
   double X[9], A[9];
 #pragma unroll
   for (int k = 0; k < 9; ++k) X[k] = S[k] - a.crest[9 * (size_t)v + k];
@@ -457,6 +452,46 @@ k_local(DevModel m, LocalArgs a) {
   }
   a.alpha0[v] = al0;
   a.kacc[v] = kv;
+}
+
+// One thread per free vertex (any number of cubature slots).
+__global__ void __launch_bounds__(128, 4)
+k_local(DevModel m, LocalArgs a) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m.nfree) return;
+  int v = m.free_list[i];
+  double S[9];
+  sampled_inner(m, a, v, S);
+  local_tail(m, a, v, S);
+}
+
+// kLocalLanes lanes per free vertex (smax <= kLocalLanes): lane s gathers and
+// contracts cubature slot s (M+, the four corner rotations and rows: the
+// dependent gathers of all slots are in flight at once instead of one
+// thread walking them), the slot sums are combined by a fixed shuffle tree,
+// and lane 0 finishes the vertex. ncu showed the one-thread form
+// long-scoreboard bound (k_local).
+constexpr int kLocalLanes = 8;
+__global__ void __launch_bounds__(128)
+k_local_lanes(DevModel m, LocalArgs a) {
+  const int g = threadIdx.x & (kLocalLanes - 1);
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) / kLocalLanes;
+  const bool live = i < m.nfree;
+  const int v = live ? m.free_list[i] : 0;
+  double X[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) X[k] = 0.0;
+  if (live && g < m.smax) {
+    size_t vs = (size_t)v * m.smax + g;
+    int u = __ldg(a.cub_u + vs);
+    if (u >= 0) sampled_slot(a, vs, u, __ldg(a.cub_w + vs), __ldg(a.cub_verts + vs), X);
+  }
+#pragma unroll
+  for (int o = kLocalLanes / 2; o > 0; o >>= 1)
+#pragma unroll
+    for (int k = 0; k < 9; ++k) X[k] += __shfl_down_sync(0xffffffffu, X[k], o, kLocalLanes);
+  if (!live || g != 0) return;
+  local_tail(m, a, v, X);
 }
 
 // Global part of the local line search: loop exit iteration and floor flag
