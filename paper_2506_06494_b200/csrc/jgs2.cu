@@ -236,11 +236,7 @@ void local_systems(Ctx& C, double* A_out, double* g_out, double* corr_out, const
     PlainArgs pa{C.mplus_all, C.z, C.dhat, C.kappa};
     if (m.nfree > 0) k_plain_local<<<grid_for(m.nfree, 128), 128, 0, C.stream>>>(m, a, pa);
   } else if (m.nfree > 0) {
-    static const bool one_thread = getenv("JGS2_LOCAL_ONE_THREAD") != nullptr;
-    if (m.smax <= kLocalLanes && !one_thread)
-      k_local_lanes<<<grid_for((int64_t)m.nfree * kLocalLanes, 128), 128, 0, C.stream>>>(m, a);
-    else
-      k_local<<<grid_for(m.nfree, 128), 128, 0, C.stream>>>(m, a);
+    k_local<<<grid_for(m.nfree, 128), 128, 0, C.stream>>>(m, a);
   }
   C.check_launch();
   // the local search's halving rounds are global (local_solver.py:539-553):

@@ -465,35 +465,6 @@ k_local(DevModel m, LocalArgs a) {
   local_tail(m, a, v, S);
 }
 
-// kLocalLanes lanes per free vertex (smax <= kLocalLanes): lane s gathers and
-// contracts cubature slot s (M+, the four corner rotations and rows: the
-// dependent gathers of all slots are in flight at once instead of one
-// thread walking them), the slot sums are combined by a fixed shuffle tree,
-// and lane 0 finishes the vertex. ncu showed the one-thread form
-// long-scoreboard bound (k_local).
-constexpr int kLocalLanes = 8;
-__global__ void __launch_bounds__(128)
-k_local_lanes(DevModel m, LocalArgs a) {
-  const int g = threadIdx.x & (kLocalLanes - 1);
-  const int i = (blockIdx.x * blockDim.x + threadIdx.x) / kLocalLanes;
-  const bool live = i < m.nfree;
-  const int v = live ? m.free_list[i] : 0;
-  double X[9];
-#pragma unroll
-  for (int k = 0; k < 9; ++k) X[k] = 0.0;
-  if (live && g < m.smax) {
-    size_t vs = (size_t)v * m.smax + g;
-    int u = __ldg(a.cub_u + vs);
-    if (u >= 0) sampled_slot(a, vs, u, __ldg(a.cub_w + vs), __ldg(a.cub_verts + vs), X);
-  }
-#pragma unroll
-  for (int o = kLocalLanes / 2; o > 0; o >>= 1)
-#pragma unroll
-    for (int k = 0; k < 9; ++k) X[k] += __shfl_down_sync(0xffffffffu, X[k], o, kLocalLanes);
-  if (!live || g != 0) return;
-  local_tail(m, a, v, X);
-}
-
 // Global part of the local line search: loop exit iteration and floor flag
 // (local_solver.py:539-552). Single thread.
 __global__ void k_ls_final(int max_halvings, double alpha_floor, const int* cnt,
