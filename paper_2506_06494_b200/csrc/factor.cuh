@@ -93,6 +93,20 @@ __global__ void k_extend_add(int nrc, const double* Uc, const int* rmap, int nsp
 // columns (backward) are split over many CTAs; fronts depend only on their
 // children (forward) / ancestors (backward), one launch per tree level.
 constexpr int kSolveThreads = 256;
+// Panel leading dimension, in doubles. The apply kernels read 64-row chunks
+// of a column; with columns aligned to 128 B (the L2 line) a chunk covers
+// whole lines. At 16-B alignment (ld even) ncu counted 10% more DRAM bytes
+// than the panels hold (profiles/r2_traffic_c4.json). Override with
+// JGS2_LD_ALIGN (2 = round-1 layout) for A/B measurements.
+constexpr int kLdAlignDefault = 16;
+inline int ld_align() {
+  static const int a = [] {
+    const char* e = getenv("JGS2_LD_ALIGN");
+    int v = e ? atoi(e) : kLdAlignDefault;
+    return (v >= 2 && (v & 1) == 0) ? v : kLdAlignDefault;
+  }();
+  return a;
+}
 constexpr int kSmemCapDoubles = 16384;  // 128 KB vector cache
 
 __global__ void k_zero_upper(int ns, int nf, double* P) {
@@ -405,7 +419,7 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
     fns[f] = 3 * (S.col_end[f] - S.col_begin[f]);
     fnr[f] = 3 * (int)(S.struct_ptr[f + 1] - S.struct_ptr[f]);
     int nf = fns[f] + fnr[f];
-    fld[f] = nf + (nf & 1);  // even leading dimension: 16-B aligned columns
+    fld[f] = (nf + ld_align() - 1) / ld_align() * ld_align();  // aligned columns (ld_align)
     loff[f + 1] = loff[f] + (int64_t)fld[f] * fns[f];
     uoff[f + 1] = uoff[f] + fnr[f];
     woff[f + 1] = woff[f] + fld[f];
