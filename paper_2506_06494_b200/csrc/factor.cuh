@@ -237,6 +237,26 @@ k_fwd_apply_narrow(const int4* tasks, int ntasks, const int* colbeg, const int* 
     const int64_t s2 = (int64_t)ld / 2;
     double a0 = 0, a1 = 0, a2 = 0, a3 = 0, c0 = 0, c1 = 0, c2 = 0, c3 = 0;
     int j = 0;
+    for (; j + 7 < cend; j += 8) {  // 8 column loads in flight per lane
+      double2 p0 = __ldg(Pr + (int64_t)j * s2);
+      double2 p1 = __ldg(Pr + (int64_t)(j + 1) * s2);
+      double2 p2 = __ldg(Pr + (int64_t)(j + 2) * s2);
+      double2 p3 = __ldg(Pr + (int64_t)(j + 3) * s2);
+      double2 p4 = __ldg(Pr + (int64_t)(j + 4) * s2);
+      double2 p5 = __ldg(Pr + (int64_t)(j + 5) * s2);
+      double2 p6 = __ldg(Pr + (int64_t)(j + 6) * s2);
+      double2 p7 = __ldg(Pr + (int64_t)(j + 7) * s2);
+      double v0 = __ldg(v + j), v1 = __ldg(v + j + 1), v2 = __ldg(v + j + 2), v3 = __ldg(v + j + 3);
+      double v4 = __ldg(v + j + 4), v5 = __ldg(v + j + 5), v6 = __ldg(v + j + 6), v7 = __ldg(v + j + 7);
+      a0 += p0.x * v0; c0 += p0.y * v0;
+      a1 += p1.x * v1; c1 += p1.y * v1;
+      a2 += p2.x * v2; c2 += p2.y * v2;
+      a3 += p3.x * v3; c3 += p3.y * v3;
+      a0 += p4.x * v4; c0 += p4.y * v4;
+      a1 += p5.x * v5; c1 += p5.y * v5;
+      a2 += p6.x * v6; c2 += p6.y * v6;
+      a3 += p7.x * v7; c3 += p7.y * v7;
+    }
     for (; j + 3 < cend; j += 4) {
       double2 p0 = __ldg(Pr + (int64_t)j * s2);
       double2 p1 = __ldg(Pr + (int64_t)(j + 1) * s2);
