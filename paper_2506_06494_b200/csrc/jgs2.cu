@@ -82,6 +82,7 @@ LocalArgs localargs(Ctx& C) {
   memset(&a, 0, sizeof(a));
   a.R = C.R; a.gasm = C.gasm; a.b = C.q; a.gbar = C.gbar; a.group = C.group; a.grows = C.grows;
   a.cub_u = C.cub_u; a.cub_w = C.cub_w; a.cub_rows = C.cub_rows; a.cub_verts = C.cub_verts;
+  a.nv = C.nv;
   a.crest = C.crest; a.mplus = C.mplus; a.h = C.h;
   a.delta = C.delta; a.alpha0 = C.alpha0; a.kacc = C.kacc;
   a.line_search = C.local_line_search ? 1 : 0;
@@ -969,7 +970,7 @@ int32_t jgs2_set_precompute(jgs2_ctx* ctx, const jgs2_precompute* p, const jgs2_
         int slot = (int)(s - p->cub_ptr[k]);
         int64_t e = p->cub_elems[s];
         if (e < 0 || e >= C.ne) throw Error(JGS2_E_ARG, "cubature element out of range");
-        size_t vs = (size_t)v * smax + slot;
+        size_t vs = (size_t)slot * nv + v;  // slot-major SoA (LocalArgs)
         cub_e[vs] = (int)e;
         cub_w[vs] = p->cub_weights[s];
         int cs[4];
@@ -981,7 +982,7 @@ int32_t jgs2_set_precompute(jgs2_ctx* ctx, const jgs2_precompute* p, const jgs2_
             throw Error(JGS2_E_KEY, "basis at vertex " + std::to_string(v) + " lacks rows for vertex " +
                                         std::to_string(w) + " of cubature element " + std::to_string(e));
           const double* blk = p->vrows + 9 * (p->vrows_ptr[k] + (it - keys));
-          for (int i = 0; i < 9; ++i) cub_rows[36 * vs + 9 * a + i] = blk[i];
+          for (int i = 0; i < 9; ++i) cub_rows[((size_t)slot * 36 + 9 * a + i) * nv + v] = blk[i];
         }
         cub_verts[vs] = make_int4(cs[0], cs[1], cs[2], cs[3]);
       }

@@ -157,10 +157,13 @@ struct LocalArgs {
   const double* gbar;       // nv*9
   const int* group;         // nv*gmax
   const double* grows;      // nv*9*gmax  (3 x 3gmax row-major)
+  // cubature slots, slot-major SoA (coalesced across the vertices of a warp):
+  // cub_u/w/verts[s * nv + v], cub_rows[(s * 36 + q) * nv + v]
   const int* cub_u;
   const double* cub_w;
   const double* cub_rows;
   const int4* cub_verts;
+  int nv;
   const double* crest;
   const double* mplus;
   double h;
@@ -287,9 +290,9 @@ __device__ double alpha_cap(const LocalArgs& a, int v, const double* d) {
 // R_i conjugation).  rows^T (R_blk H_rest R_blk^T) rows = R_i V^T H_rest V R_i^T
 // because R_w^T R_w = I, so the rest part is the precomputed C_v.
 // One cubature slot: E = sum_k Had(k,:) (x) R_{w_k} rows_k, X += w E^T M+ E.
-__device__ __forceinline__ void sampled_slot(const LocalArgs& a, size_t vs, int u, double w, int4 cv,
+__device__ __forceinline__ void sampled_slot(const LocalArgs& a, int v, int s, int u, double w, int4 cv,
                                              double* X) {
-  const double* rows = a.cub_rows + 36 * vs;
+  const double* rows = a.cub_rows + (size_t)s * 36 * a.nv + v;  // rows[q * nv]
   const double* M = a.mplus + 45 * (size_t)u;
   double E[27];
 #pragma unroll
@@ -297,8 +300,10 @@ __device__ __forceinline__ void sampled_slot(const LocalArgs& a, size_t vs, int 
   int corner[4] = {cv.x, cv.y, cv.z, cv.w};
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    double Bk[9];
-    mat3_mul(a.R + 9 * (size_t)corner[k], rows + 9 * k, Bk);
+    double Bk[9], rk[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) rk[q] = __ldg(rows + (size_t)(9 * k + q) * a.nv);
+    mat3_mul(a.R + 9 * (size_t)corner[k], rk, Bk);
 #pragma unroll
     for (int p = 0; p < 3; ++p) {
       double hw = kHad(k, p);
@@ -343,24 +348,21 @@ __device__ void sampled_inner(const DevModel& m, const LocalArgs& a, int v, doub
     for (int s = 0; s < kSlotsHoisted; ++s) {
       us[s] = -1;
       if (s < m.smax) {
-        size_t vs = (size_t)v * m.smax + s;
+        size_t vs = (size_t)s * a.nv + v;
         us[s] = __ldg(a.cub_u + vs);
         cvs[s] = __ldg(a.cub_verts + vs);
       }
     }
 #pragma unroll 1
     for (int s = 0; s < m.smax; ++s)
-      if (us[s] >= 0) {
-        size_t vs = (size_t)v * m.smax + s;
-        sampled_slot(a, vs, us[s], __ldg(a.cub_w + vs), cvs[s], X);
-      }
+      if (us[s] >= 0) sampled_slot(a, v, s, us[s], __ldg(a.cub_w + (size_t)s * a.nv + v), cvs[s], X);
     return;
   }
   for (int s = 0; s < m.smax; ++s) {
-    size_t vs = (size_t)v * m.smax + s;
+    size_t vs = (size_t)s * a.nv + v;
     int u = a.cub_u[vs];
     if (u < 0) continue;
-    sampled_slot(a, vs, u, a.cub_w[vs], a.cub_verts[vs], X);
+    sampled_slot(a, v, s, u, a.cub_w[vs], a.cub_verts[vs], X);
   }
 }
 
