@@ -366,6 +366,16 @@ def main():
     e2e = (e2e_sweeps / replicas.max_over_ranks(dist, e2e_s) if partitioned
            else replicas.job_throughput(dist, e2e_sweeps, e2e_s))
 
+    fill = None
+    if rank == 0:
+        try:
+            t0 = time.perf_counter()
+            stored, nd_exact, metis = solver.factor_fill()
+            fill = {"nnz_L_stored": stored, "nnz_L_nd_exact": nd_exact, "nnz_L_metis_exact": metis,
+                    "nd_over_metis": nd_exact / metis, "seconds": round(time.perf_counter() - t0, 1)}
+        except Exception as exc:
+            fill = {"failed": str(exc)}
+
     # the scalable precompute at this config, and sweeps driven
     # by it: the reference algorithm's own bases/cubature instead of the
     # injected ones (rank 0 only, after the timed windows)
@@ -409,7 +419,9 @@ def main():
                      "mean_sweeps_per_frame": float(np.mean([it for it, _, _ in ts])) if ts else None,
                      "frames_completed_in_window": frames_done},
         "factor": {"nnz_L": int(fi.nnz_dof), "fronts": int(fi.nfronts), "levels": int(fi.nlevels),
-                   "max_front": int(fi.max_front), "ordering": "geometric nested dissection",
+                   "max_front": int(fi.max_front),
+                   "ordering": "METIS nested dissection" if fi.ordering == 1 else "geometric nested dissection",
+                   "fill_vs_metis": fill,
                    "factor_s": round(solver.factor_seconds, 2), "precompute_s": round(t_pre, 2)},
         "roofline": {"bound": "hbm", "kernel": dom,
                      "dominant_phase": max(phases, key=lambda p: phases[p][0]), "achieved": achieved, "peak": peak,

@@ -112,6 +112,7 @@ typedef struct jgs2_factor_info {
   int64_t nlevels;
   int64_t max_front;       /* largest front order (DOFs) */
   double factor_seconds;
+  int64_t ordering;        /* 1 METIS nested dissection (default), 0 geometric nested dissection */
 } jgs2_factor_info;
 
 /* ---- lifecycle ------------------------------------------------------- */
@@ -137,6 +138,12 @@ int32_t jgs2_factor_rest(jgs2_ctx* ctx, double h_ref, int32_t leaf_size, jgs2_fa
  * touching fixed vertices are ignored (their rows are identity). */
 int32_t jgs2_factor_blocks(jgs2_ctx* ctx, int64_t nblocks, const int64_t* brow, const int64_t* bcol,
                            const double* bval, int32_t leaf_size, jgs2_factor_info* info);
+
+/* Fill of the factor: out[0] = stored supernodal entries (DOF units, the
+ * bytes the solve streams), out[1] = exact Cholesky fill of the same
+ * geometric nested-dissection ordering, out[2] = exact fill of METIS nested
+ * dissection (cusolverSpXcsrmetisndHost) on the same graph. */
+int32_t jgs2_factor_fill(jgs2_ctx* ctx, int64_t* out);
 
 /* ---- state ----------------------------------------------------------- */
 int32_t jgs2_set_state(jgs2_ctx* ctx, const double* x, const double* z, double h);

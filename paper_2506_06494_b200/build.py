@@ -15,7 +15,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "lib"
 LIB = LIBDIR / "libjgs2.so"
-SOURCES = ["jgs2.cu", "symbolic.cpp"]
+SOURCES = ["jgs2.cu", "symbolic.cpp", "fill.cpp"]
 HEADERS = sorted(p.name for p in CSRC.glob("*.cuh")) + ["symbolic.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -68,7 +68,7 @@ def build(force=False, verbose=False):
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "-Xptxas", "-O3", "-Xcompiler", "-fopenmp", "-I", str(PKG.parent / "include"), "-I", str(ninc),
            *[str(CSRC / s) for s in SOURCES], "-o", str(tmp),
-           "-L", str(libdir), f"-Xlinker=-rpath,{libdir}", "-lcusolver", "-lcublas",
+           "-L", str(libdir), f"-Xlinker=-rpath,{libdir}", "-lcusolver", "-lcublas", "-lcusparse",
            "-L", str(nlib), f"-Xlinker=-rpath,{nlib}", "-l:libnccl.so.2", "-lgomp"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")

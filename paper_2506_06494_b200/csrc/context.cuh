@@ -83,6 +83,7 @@ struct Comm {
 // Device-side factor of the free-vertex rest Hessian (supernodal, ND order).
 struct Factor {
   bool ready = false;
+  bool ordering_metis = false;
   Symbolic sym;
   int nfree = 0;
   int nfronts = 0, nlevels = 0;

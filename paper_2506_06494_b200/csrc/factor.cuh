@@ -380,6 +380,9 @@ struct BlockInput {
   const double* bval;
 };
 
+void metis_nd(int n, const int64_t* ptr, const int32_t* adj, int32_t* p);  // fill.cpp
+constexpr bool kDefaultMetis = true;
+
 // Build the factor of the free-vertex rest Hessian on the device: either
 // assembled from the model at h_ref (blocks == nullptr) or from caller blocks.
 void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nullptr) {
@@ -426,7 +429,21 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
   std::vector<double> coords(3 * (size_t)n);
   for (int i = 0; i < n; ++i)
     for (int c = 0; c < 3; ++c) coords[3 * (size_t)i + c] = C.h_rest[3 * (size_t)glob[i] + c];
-  build_symbolic(n, aptr.data(), adj.data(), coords.data(), leaf, F.sym);
+  // ordering: METIS nested dissection (cusolverSpXcsrmetisndHost, fill.cpp)
+  // with an etree-based front tree, or geometric nested dissection
+  // (symbolic.cpp); JGS2_ORDERING=metis|geometric, JGS2_RELAX = amalgamation
+  // limit in vertices
+  static const char* ord_env = getenv("JGS2_ORDERING");
+  const bool use_metis = ord_env ? std::string(ord_env) == "metis" : kDefaultMetis;
+  F.ordering_metis = use_metis;
+  if (use_metis && n > 0) {
+    std::vector<int32_t> pm(n);
+    metis_nd(n, aptr.data(), adj.data(), pm.data());
+    static const char* rx = getenv("JGS2_RELAX");
+    build_symbolic_perm(n, aptr.data(), adj.data(), pm.data(), rx ? atoi(rx) : 32, F.sym);
+  } else {
+    build_symbolic(n, aptr.data(), adj.data(), coords.data(), leaf, F.sym);
+  }
   Symbolic& S = F.sym;
   F.nfronts = S.nfronts;
   F.nlevels = S.nlevels;

@@ -20,6 +20,10 @@
 #include "train.cuh"
 #include "plain.cuh"
 
+namespace jgs2 {  // fill.cpp
+int64_t chol_nnz(int n, const int64_t* ptr, const int32_t* adj, const int32_t* p);
+}  // namespace jgs2
+
 using namespace jgs2;
 
 jgs2::Ctx::~Ctx() {
@@ -1090,6 +1094,7 @@ int32_t jgs2_factor_rest(jgs2_ctx* ctx, double h_ref, int32_t leaf_size, jgs2_fa
       info->nlevels = C.fac.nlevels;
       info->max_front = C.fac.max_nf;
       info->factor_seconds = C.fac.seconds;
+      info->ordering = C.fac.ordering_metis ? 1 : 0;
     }
   });
 }
@@ -1108,6 +1113,7 @@ int32_t jgs2_factor_blocks(jgs2_ctx* ctx, int64_t nblocks, const int64_t* brow, 
       info->nlevels = C.fac.nlevels;
       info->max_front = C.fac.max_nf;
       info->factor_seconds = C.fac.seconds;
+      info->ordering = C.fac.ordering_metis ? 1 : 0;
     }
   });
 }
@@ -1466,6 +1472,48 @@ int32_t jgs2_local_step(jgs2_ctx* ctx, double* delta, double* alpha, int64_t* ac
     JGS2_CUDA(cudaFreeAsync(dal, C.stream));
     C.sync();
     if (activations) *activations = C.local_line_search ? lsf[2] : 0;
+  });
+}
+
+int32_t jgs2_factor_fill(jgs2_ctx* ctx, int64_t* out) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (!C.fac.ready) throw Error(JGS2_E_ARG, "rest factor not built");
+    const Symbolic& S = C.fac.sym;
+    const int n = S.n;
+    // the factored free-vertex graph (vertex adjacency through elements)
+    // node ids of the symbolic graph: node = perm[pos]; pos = h_pos[v]
+    std::vector<int> node_of(C.nv, -1);
+    for (int v = 0; v < C.nv; ++v)
+      if (C.fac.h_pos[v] >= 0) node_of[v] = S.perm[C.fac.h_pos[v]];
+    std::vector<std::vector<int>> nb(n);
+    for (int e = 0; e < C.ne; ++e) {
+      const int64_t* t = &C.h_tets[4 * (size_t)e];
+      for (int a = 0; a < 4; ++a) {
+        int na = node_of[t[a]];
+        if (na < 0) continue;
+        for (int b = 0; b < 4; ++b) {
+          int nbb = node_of[t[b]];
+          if (nbb >= 0 && nbb != na) nb[na].push_back(nbb);
+        }
+      }
+    }
+    std::vector<int64_t> ptr(n + 1, 0);
+    std::vector<int32_t> adj;
+    for (int i = 0; i < n; ++i) {
+      auto& s = nb[i];
+      std::sort(s.begin(), s.end());
+      s.erase(std::unique(s.begin(), s.end()), s.end());
+      adj.insert(adj.end(), s.begin(), s.end());
+      ptr[i + 1] = (int64_t)adj.size();
+    }
+    auto dof = [n](int64_t lv) { return 9 * (lv - n) + 6 * (int64_t)n; };  // 3x3 blocks, lower
+    std::vector<int32_t> pnd(S.perm.begin(), S.perm.end()), pm(n);
+    int64_t nd_exact = chol_nnz(n, ptr.data(), adj.data(), pnd.data());
+    metis_nd(n, ptr.data(), adj.data(), pm.data());
+    int64_t metis_exact = chol_nnz(n, ptr.data(), adj.data(), pm.data());
+    out[0] = S.nnz_dof;        // the solve's supernodal storage (dense diagonal blocks)
+    out[1] = dof(nd_exact);    // exact Cholesky fill of the same ordering
+    out[2] = dof(metis_exact); // exact Cholesky fill of METIS nested dissection
   });
 }
 

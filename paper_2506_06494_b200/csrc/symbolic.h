@@ -36,4 +36,10 @@ struct Symbolic {
 void build_symbolic(int n, const int64_t* adj_ptr, const int32_t* adj, const double* coords,
                     int leaf_size, Symbolic& out);
 
+// Front tree from a given ordering perm (perm[pos] = node), e.g. METIS
+// nested dissection: etree postorder, fundamental supernodes, relaxed
+// amalgamation up to `relax` vertices per merged front.
+void build_symbolic_perm(int n, const int64_t* adj_ptr, const int32_t* adj, const int32_t* perm, int relax,
+                         Symbolic& out);
+
 }  // namespace jgs2

@@ -280,6 +280,13 @@ class LocalSolver:
         return int(n.value)
 
     # ------------------------------------------------------------ measurement
+    def factor_fill(self):
+        """(stored supernodal nnz, exact fill of the same ordering, exact fill
+        of METIS nested dissection), DOF units (jgs2_factor_fill)."""
+        out = np.zeros(3, dtype=np.int64)
+        self._call(self._lib.jgs2_factor_fill, L.ptr(out, L.i64))
+        return tuple(int(x) for x in out)
+
     def profile(self, enable=True):
         self._call(self._lib.jgs2_profile, int(bool(enable)))
 
