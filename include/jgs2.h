@@ -128,6 +128,12 @@ int32_t jgs2_set_precompute(jgs2_ctx* ctx, const jgs2_precompute* pre, const jgs
  * first-fit in ascending vertex id, mesh.py:164-178; nv entries): free
  * vertices are updated colour by colour, ascending (local_solver.py:298-303). */
 int32_t jgs2_set_colors(jgs2_ctx* ctx, const int64_t* colors);
+/* Fill-reducing ordering of the next factorization: 1 = METIS nested
+ * dissection (cusolverSpXcsrmetisndHost) with an elimination-tree front tree,
+ * fronts amalgamated up to leaf_size vertices (the default); 0 = geometric
+ * nested dissection with leaves of leaf_size vertices (the scalable
+ * precompute's large fronts). */
+int32_t jgs2_set_ordering(jgs2_ctx* ctx, int32_t ordering);
 /* Rest Hessian M/h^2 + PSD elastic, Dirichlet-eliminated, factored on the
  * device (replaces subspace.rest_factorization, subspace.py:126-130). */
 int32_t jgs2_factor_rest(jgs2_ctx* ctx, double h_ref, int32_t leaf_size, jgs2_factor_info* info);

@@ -345,6 +345,7 @@ struct Ctx {
   }
 
   Factor fac;
+  int ordering = -1;           // jgs2_set_ordering: 1 METIS ND, 0 geometric ND, -1 default (METIS)
   std::shared_ptr<struct TrainOut> train;  // scalable precompute output (train.cuh)
   cublasHandle_t cublas = nullptr;
   cusolverDnHandle_t cusolver = nullptr;

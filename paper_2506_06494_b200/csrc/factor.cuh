@@ -434,13 +434,14 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
   // (symbolic.cpp); JGS2_ORDERING=metis|geometric, JGS2_RELAX = amalgamation
   // limit in vertices
   static const char* ord_env = getenv("JGS2_ORDERING");
-  const bool use_metis = ord_env ? std::string(ord_env) == "metis" : kDefaultMetis;
+  const bool use_metis = ord_env ? std::string(ord_env) == "metis"
+                                 : (C.ordering >= 0 ? C.ordering == 1 : kDefaultMetis);
   F.ordering_metis = use_metis;
   if (use_metis && n > 0) {
     std::vector<int32_t> pm(n);
     metis_nd(n, aptr.data(), adj.data(), pm.data());
     static const char* rx = getenv("JGS2_RELAX");
-    build_symbolic_perm(n, aptr.data(), adj.data(), pm.data(), rx ? atoi(rx) : 32, F.sym);
+    build_symbolic_perm(n, aptr.data(), adj.data(), pm.data(), rx ? atoi(rx) : leaf, F.sym);
   } else {
     build_symbolic(n, aptr.data(), adj.data(), coords.data(), leaf, F.sym);
   }

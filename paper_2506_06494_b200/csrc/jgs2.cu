@@ -1081,6 +1081,14 @@ int32_t jgs2_set_colors(jgs2_ctx* ctx, const int64_t* colors) {
   });
 }
 
+int32_t jgs2_set_ordering(jgs2_ctx* ctx, int32_t ordering) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (ordering != 0 && ordering != 1) throw Error(JGS2_E_ARG, "ordering must be 0 (geometric) or 1 (METIS)");
+    if (C.fac.ready) throw Error(JGS2_E_ARG, "factor already built");
+    C.ordering = ordering;
+  });
+}
+
 int32_t jgs2_factor_rest(jgs2_ctx* ctx, double h_ref, int32_t leaf_size, jgs2_factor_info* info) {
   return guarded(ctx, [&](Ctx& C) {
     if (!C.have_model) throw Error(JGS2_E_ARG, "set the model first");

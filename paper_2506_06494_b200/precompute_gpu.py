@@ -48,6 +48,9 @@ def scalable_precompute(model, h_ref, *, max_size=6, training_poses=2, amplitude
         upload_model(lib, ctx, model, keep)
         t0 = time.perf_counter()
         fi = L.FactorInfo()
+        # geometric nested dissection with large leaves: each vertex's front (the
+        # rows the selected inverse provides, the cubature pool) is its leaf cell
+        L.check(lib.jgs2_set_ordering(ctx, 0), ctx)
         L.check(lib.jgs2_factor_rest(ctx, float(h_ref), int(leaf_size), C.byref(fi)), ctx)
         info["factor_s"] = time.perf_counter() - t0
         info["nnz_L"] = int(fi.nnz_dof)

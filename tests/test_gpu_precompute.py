@@ -22,7 +22,7 @@ def _ctx_with_selinv(model, h):
     keep = []
     upload_model(lib, ctx, model, keep)
     fi = L.FactorInfo()
-    L.check(lib.jgs2_factor_rest(ctx, h, 32, C.byref(fi)), ctx)
+    L.check(lib.jgs2_factor_rest(ctx, h, 32, C.byref(fi)), ctx)  # METIS ordering (default)
     L.check(lib.jgs2_selected_inverse(ctx, None), ctx)
     return lib, ctx
 
