@@ -146,9 +146,9 @@ int32_t jgs2_factor_blocks(jgs2_ctx* ctx, int64_t nblocks, const int64_t* brow, 
                            const double* bval, int32_t leaf_size, jgs2_factor_info* info);
 
 /* Fill of the factor: out[0] = stored supernodal entries (DOF units, the
- * bytes the solve streams), out[1] = exact Cholesky fill of the same
- * geometric nested-dissection ordering, out[2] = exact fill of METIS nested
- * dissection (cusolverSpXcsrmetisndHost) on the same graph. */
+ * bytes the solve streams), out[1] = exact Cholesky fill of the factor's own
+ * ordering, out[2] = exact fill of METIS nested dissection
+ * (cusolverSpXcsrmetisndHost) of the whole graph. */
 int32_t jgs2_factor_fill(jgs2_ctx* ctx, int64_t* out);
 
 /* ---- state ----------------------------------------------------------- */

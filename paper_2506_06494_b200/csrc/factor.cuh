@@ -381,6 +381,7 @@ struct BlockInput {
 };
 
 void metis_nd(int n, const int64_t* ptr, const int32_t* adj, int32_t* p);  // fill.cpp
+void metis_nd_components(int n, const int64_t* ptr, const int32_t* adj, int32_t* p);
 constexpr bool kDefaultMetis = true;
 
 // Build the factor of the free-vertex rest Hessian on the device: either
@@ -439,7 +440,7 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
   F.ordering_metis = use_metis;
   if (use_metis && n > 0) {
     std::vector<int32_t> pm(n);
-    metis_nd(n, aptr.data(), adj.data(), pm.data());
+    metis_nd_components(n, aptr.data(), adj.data(), pm.data());
     static const char* rx = getenv("JGS2_RELAX");
     build_symbolic_perm(n, aptr.data(), adj.data(), pm.data(), rx ? atoi(rx) : leaf, F.sym);
   } else {

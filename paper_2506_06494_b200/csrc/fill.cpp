@@ -4,6 +4,7 @@
 #include <cusolverSp.h>
 #include <cusparse.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <stdexcept>
 #include <vector>
@@ -73,6 +74,50 @@ void metis_nd(int n, const int64_t* ptr, const int32_t* adj, int32_t* p) {
   cusparseDestroyMatDescr(d);
   cusolverSpDestroy(h);
   if (st != CUSOLVER_STATUS_SUCCESS) throw std::runtime_error("cusolverSpXcsrmetisndHost failed");
+}
+
+// METIS nested dissection of each connected component on its own,
+// components concatenated in order of their smallest node. A body's ordering
+// (and so its factor, bit for bit) does not depend on the other bodies in
+// the graph: a partitioned solve factoring a subset of the bodies
+// reproduces the single-GPU factor of each.
+void metis_nd_components(int n, const int64_t* ptr, const int32_t* adj, int32_t* p) {
+  std::vector<int> comp(n, -1), order;
+  order.reserve(n);
+  int out = 0;
+  std::vector<int64_t> cptr;
+  std::vector<int32_t> cadj;
+  std::vector<int> loc(n, -1);
+  for (int s = 0; s < n; ++s) {
+    if (comp[s] >= 0) continue;
+    order.clear();
+    order.push_back(s);
+    comp[s] = s;
+    for (size_t h = 0; h < order.size(); ++h) {
+      int u = order[h];
+      for (int64_t q = ptr[u]; q < ptr[u + 1]; ++q) {
+        int w = adj[q];
+        if (comp[w] < 0) { comp[w] = s; order.push_back(w); }
+      }
+    }
+    std::sort(order.begin(), order.end());  // component nodes ascending
+    const int m = (int)order.size();
+    for (int k = 0; k < m; ++k) loc[order[k]] = k;
+    cptr.assign(m + 1, 0);
+    cadj.clear();
+    for (int k = 0; k < m; ++k) {
+      int u = order[k];
+      for (int64_t q = ptr[u]; q < ptr[u + 1]; ++q) cadj.push_back(loc[adj[q]]);
+      cptr[k + 1] = (int64_t)cadj.size();
+    }
+    std::vector<int32_t> cp(m);
+    if (m <= 2) {
+      for (int k = 0; k < m; ++k) cp[k] = k;
+    } else {
+      metis_nd(m, cptr.data(), cadj.data(), cp.data());
+    }
+    for (int k = 0; k < m; ++k) p[out++] = order[cp[k]];
+  }
 }
 
 }  // namespace jgs2
