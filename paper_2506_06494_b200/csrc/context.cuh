@@ -109,6 +109,12 @@ struct Factor {
   int4* fwdn_tasks = nullptr;  // narrow fronts: (front, 64-row chunk)
   std::vector<int> fwdn_level_ptr;
   int4* bwd_tasks = nullptr;   // (front, col_begin, col_end)
+  int4* bwdn_tasks = nullptr;  // narrow fronts: (front, <= 8 columns)
+  std::vector<int> bwdn_level_ptr;
+  struct SplitTask* split_tasks = nullptr;  // top levels: (64-row block, column chunk)
+  std::vector<int> split_level_ptr;
+  double* split_part = nullptr;
+  unsigned* split_ticket = nullptr;
   std::vector<int> fwd_level_ptr, bwd_level_ptr, fwd_level_smem, bwd_level_smem;
   std::vector<int64_t> asm_level_ptr, gat_level_ptr;
   int64_t* asm_dst = nullptr;  // flat forward assembly map
@@ -208,6 +214,8 @@ struct Ctx {
   int* hess_count = nullptr;   // indefinite-element count (pass 1 -> pass 2)
   int* hess_list = nullptr;    // compacted indefinite elements
   cudaStream_t stream2 = nullptr;  // side stream for the element-Hessian passes
+  cudaStream_t solve_side = nullptr;  // factor solve: a level's narrow launches beside the wide ones
+  cudaEvent_t ev_sfork = nullptr, ev_sjoin = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool hess_pending = false;
   // retained rows CSR for contact coupling rows (local_solver.py:85-112)

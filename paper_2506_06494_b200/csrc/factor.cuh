@@ -212,12 +212,125 @@ k_fwd_apply(const int4* tasks, int ntasks, const int* colbeg, const int* f_ns, c
   }
 }
 
+// forward apply on the top levels, where a few wide fronts give too few row
+// tasks to fill the GPU (65-189 CTAs measured on C4: 0.8-2.6 TB/s). A task is
+// (64-row block, column chunk); every chunk writes its partial rows to
+// scratch, and the last chunk of a row block to finish (atomic ticket) sums
+// the partials in chunk order (deterministic) and writes z / u. The ticket
+// is reset by that last chunk, so the captured graph replays.
+struct SplitTask {
+  int f, r0, c0, c1;      // rows [r0, r0 + 64), columns [c0, c1)
+  int slot, nk, k, blk;   // partials at part[(slot + k) * 64], nk chunks, ticket blk
+};
+constexpr int kSplitMaxCols = 2048;
+__global__ void __launch_bounds__(kSolveThreads, kApplyCtasPerSm)
+k_fwd_apply_split(const SplitTask* tasks, int ntasks, const int* colbeg, const int* f_ns, const int* f_nr,
+                  const int* f_ld, const int64_t* loff, const int64_t* uoff, const int64_t* woff,
+                  const double* __restrict__ L, const double* __restrict__ w, double* b, double* u,
+                  double* part, unsigned* ticket) {
+  __shared__ double sv[kSplitMaxCols];
+  __shared__ double red[8][65];
+  __shared__ int last;
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
+    SplitTask tk = tasks[t];
+    int f = tk.f, r0 = tk.r0, c0 = tk.c0;
+    int ns = f_ns[f], nf = ns + f_nr[f], ld = f_ld[f];
+    int r1 = min(nf, r0 + 64);
+    int c1 = min(tk.c1, min(ns, r1));
+    const double* P = L + loff[f];
+    const double* v = w + woff[f];
+    __syncthreads();  // previous task done with sv / red
+    for (int i = threadIdx.x; i < c1 - c0; i += blockDim.x) sv[i] = v[c0 + i];
+    __syncthreads();
+    int row = r0 + 2 * lane;
+    double a0 = 0, a1 = 0, a2 = 0, a3 = 0, b0 = 0, b1 = 0, b2 = 0, b3 = 0;
+    if (row < r1) {
+      const double2* Pr = reinterpret_cast<const double2*>(P + row);
+      const int64_t s = (int64_t)ld / 2;
+      int j = c0 + warp;
+      for (; j + 24 < c1; j += 32) {
+        double2 p0 = __ldg(Pr + (int64_t)j * s);
+        double2 p1 = __ldg(Pr + (int64_t)(j + 8) * s);
+        double2 p2 = __ldg(Pr + (int64_t)(j + 16) * s);
+        double2 p3 = __ldg(Pr + (int64_t)(j + 24) * s);
+        double v0 = sv[j - c0], v1 = sv[j + 8 - c0], v2 = sv[j + 16 - c0], v3 = sv[j + 24 - c0];
+        a0 += p0.x * v0; b0 += p0.y * v0;
+        a1 += p1.x * v1; b1 += p1.y * v1;
+        a2 += p2.x * v2; b2 += p2.y * v2;
+        a3 += p3.x * v3; b3 += p3.y * v3;
+      }
+      for (; j < c1; j += 8) {
+        double2 p0 = __ldg(Pr + (int64_t)j * s);
+        double v0 = sv[j - c0];
+        a0 += p0.x * v0; b0 += p0.y * v0;
+      }
+    }
+    red[warp][2 * lane] = (a0 + a1) + (a2 + a3);
+    red[warp][2 * lane + 1] = (b0 + b1) + (b2 + b3);
+    __syncthreads();
+    int r = r0 + threadIdx.x;  // threads 0-63 own one row each
+    double tt = 0.0;
+    if (threadIdx.x < 64) {
+      int c = threadIdx.x;
+      tt = ((red[0][c] + red[1][c]) + (red[2][c] + red[3][c])) +
+           ((red[4][c] + red[5][c]) + (red[6][c] + red[7][c]));
+    }
+    if (tk.nk == 1) {
+      if (threadIdx.x < 64 && r < r1) {
+        if (r < ns) b[colbeg[f] + r] = tt;
+        else u[uoff[f] + (r - ns)] = v[r] - tt;
+      }
+      continue;
+    }
+    if (threadIdx.x < 64) part[(int64_t)(tk.slot + tk.k) * 64 + threadIdx.x] = tt;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = (atomicAdd(ticket + tk.blk, 1u) == (unsigned)tk.nk - 1);
+    __syncthreads();
+    if (!last) continue;
+    __threadfence();
+    if (threadIdx.x < 64 && r < r1) {
+      double acc = 0.0;
+      for (int k = 0; k < tk.nk; ++k) acc += __ldcg(part + (int64_t)(tk.slot + k) * 64 + threadIdx.x);
+      if (r < ns) b[colbeg[f] + r] = acc;
+      else u[uoff[f] + (r - ns)] = v[r] - acc;
+    }
+    if (threadIdx.x == 0) ticket[tk.blk] = 0u;
+  }
+}
+
 // forward apply for narrow fronts (ns <= kNarrowCols: the leaves and the
 // small separators of the lower levels), task = (front, 64-row chunk): one
 // warp per task, lanes own row pairs across all columns, v broadcast from
 // L1. No shared memory and no block barriers (the block-level kernel's
 // per-64-row cross-warp reduction dominates on narrow panels).
 constexpr int kNarrowCols = 128;
+// A/B switches for the solve schedule (measurements in DESIGN.md §4):
+// JGS2_BWD_NARROW=0 runs narrow fronts' backward step in the block kernel,
+// JGS2_SOLVE_FORK=0 serialises a level's narrow and wide launches.
+inline bool env_on(const char* name) {
+  const char* e = getenv(name);
+  return !(e && e[0] == '0');
+}
+// narrow backward tasks only for short fronts: a tall narrow front (a small
+// separator high in the tree) streams each column from one warp, where the
+// block kernel puts 8 warps on it. JGS2_BWD_NARROW=<rows> (0 = off).
+inline int narrow_bwd_rows() {
+  static const int v = [] {
+    const char* e = getenv("JGS2_BWD_NARROW");
+    return e ? atoi(e) : 512;
+  }();
+  return v;
+}
+inline bool split_fwd() {
+  static const bool v = env_on("JGS2_SPLIT_FWD");
+  return v;
+}
+inline bool solve_fork() {
+  static const bool v = env_on("JGS2_SOLVE_FORK");
+  return v;
+}
 __global__ void __launch_bounds__(kSolveThreads)
 k_fwd_apply_narrow(const int4* tasks, int ntasks, const int* colbeg, const int* f_ns, const int* f_nr,
                    const int* f_ld, const int64_t* loff, const int64_t* uoff, const int64_t* woff,
@@ -370,6 +483,66 @@ k_bwd_apply(const int4* tasks, int ntasks, const int* colbeg, const int* f_ns, c
   }
 }
 
+// backward apply for narrow fronts (ns <= kNarrowCols), task = (front, group of
+// <= 8 columns): one warp per task, no shared memory and no block barriers
+// (the block kernel's per-task vector staging and 8-warp split left most warps
+// idle on these short columns: 0.9-2.5 TB/s on the lower levels). Lanes own
+// row pairs and keep the group's 8 column loads in flight; column j starts at
+// its even row at or above the diagonal. The 8 sums are reduced by a
+// transposing butterfly (9 shuffles, fixed order: deterministic).
+__global__ void __launch_bounds__(kSolveThreads)
+k_bwd_apply_narrow(const int4* tasks, int ntasks, const int* colbeg, const int* f_ns, const int* f_nr,
+                   const int* f_ld, const int64_t* loff, const int64_t* woff, const double* __restrict__ L,
+                   const double* __restrict__ w, double* q) {
+  const unsigned full = 0xffffffffu;
+  int lane = threadIdx.x & 31;
+  int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = w0; t < ntasks; t += nw) {
+    int4 tk = tasks[t];
+    int f = tk.x, c0 = tk.y, c1 = tk.z;
+    int nf = f_ns[f] + f_nr[f], ld = f_ld[f];
+    const double* P = L + loff[f] + (int64_t)c0 * ld;
+    const double2* wf = reinterpret_cast<const double2*>(w + woff[f]);
+    int nc = c1 - c0;
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = 0.0;
+    for (int i = (c0 & ~1) + 2 * lane; i < nf; i += 64) {
+      // all 8 loads issued before any use (a guarded load-use pair per
+      // column compiled to one load in flight per warp)
+      double2 p[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        p[k] = (k < nc && i + 1 >= c0 + k) ? __ldg(reinterpret_cast<const double2*>(P + (int64_t)k * ld + i))
+                                           : make_double2(0.0, 0.0);
+      double2 wv = __ldg(wf + (i >> 1));
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] += p[k].x * wv.x + p[k].y * wv.y;
+    }
+    // lane bit 4 selects columns 0-3 / 4-7, bit 3 pairs, bit 2 the column
+    bool h = lane & 16;
+    double b4[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      double send = h ? a[k] : a[k + 4], keep = h ? a[k + 4] : a[k];
+      b4[k] = keep + __shfl_xor_sync(full, send, 16);
+    }
+    h = lane & 8;
+    double b2[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      double send = h ? b4[k] : b4[k + 2], keep = h ? b4[k + 2] : b4[k];
+      b2[k] = keep + __shfl_xor_sync(full, send, 8);
+    }
+    h = lane & 4;
+    double s = (h ? b2[1] : b2[0]) + __shfl_xor_sync(full, h ? b2[0] : b2[1], 4);
+    s += __shfl_xor_sync(full, s, 2);
+    s += __shfl_xor_sync(full, s, 1);
+    int k = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+    if ((lane & 3) == 0 && k < nc) q[colbeg[f] + c0 + k] = s;
+  }
+}
+
 // ------------------------------------------------------------------ host side
 inline void factor_release(Ctx& C) { C.fac = Factor(); }
 
@@ -505,10 +678,15 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
   // multiples of 32 rows) / column blocks (backward, multiples of 8
   // columns) of roughly equal entry counts; enough tasks to fill 2 waves.
   {
-    std::vector<int4> ft, bt, fn;
+    std::vector<int4> ft, bt, fn, bn;
+    std::vector<SplitTask> st;
+    std::vector<int> wide;
+    int split_blocks = 0, split_slots = 0;
+    F.split_level_ptr.assign(F.nlevels + 1, 0);
     F.fwd_level_ptr.assign(F.nlevels + 1, 0);
     F.fwdn_level_ptr.assign(F.nlevels + 1, 0);
     F.bwd_level_ptr.assign(F.nlevels + 1, 0);
+    F.bwdn_level_ptr.assign(F.nlevels + 1, 0);
     F.fwd_level_smem.assign(F.nlevels, 0);
     F.bwd_level_smem.assign(F.nlevels, 0);
     for (int l = 0; l < F.nlevels; ++l) {
@@ -529,6 +707,7 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
           for (int i0 = 0; i0 < nf; i0 += 64) fn.push_back(make_int4(f, i0, std::min(nf, i0 + 64), 0));
           r0 = nf;
         }
+        if (r0 < nf) wide.push_back(f);
         for (int i0 = r0; i0 < nf; i0 += 64) {
           int rows = std::min(64, nf - i0);
           int cols = std::min(ns, i0 + 64);
@@ -544,6 +723,10 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
         // backward columns
         int c0 = 0;
         acc = 0;
+        if (ns <= kNarrowCols && nf <= narrow_bwd_rows()) {  // narrow front: one warp task per 8 columns
+          for (int j = 0; j < ns; j += 8) bn.push_back(make_int4(f, j, std::min(ns, j + 8), 0));
+          continue;
+        }
         for (int j = 0; j < ns; j += 8) {
           int cols = std::min(8, ns - j);
           acc += (double)cols * (nf - j);
@@ -556,12 +739,43 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
           }
         }
       }
+      // too few row tasks to fill the GPU: (64-row block, column chunk) tasks
+      int nrow = (int)ft.size() - F.fwd_level_ptr[l];
+      if (split_fwd() && nrow > 0 && nrow < 148 * kApplyCtasPerSm / 2) {
+        ft.resize(F.fwd_level_ptr[l]);
+        double ent = 0;
+        for (int f : wide) {
+          double ns = fns[f], nf = fns[f] + fnr[f];
+          ent += ns * (ns + 1) / 2 + (nf - ns) * ns;
+        }
+        int W = (int)(ent / (64.0 * 2 * 148 * kApplyCtasPerSm)) / 64 * 64;
+        W = std::min(std::max(W, 256), kSplitMaxCols);
+        for (int f : wide) {
+          int ns = fns[f], nf = fns[f] + fnr[f];
+          for (int i0 = 0; i0 < nf; i0 += 64) {
+            int cmax = std::min(ns, i0 + 64);
+            int nk = std::max(1, (cmax + W - 1) / W);
+            int blk = nk > 1 ? split_blocks++ : -1;
+            int slot = nk > 1 ? split_slots : -1;
+            if (nk > 1) split_slots += nk;
+            for (int k = 0; k < nk; ++k)
+              st.push_back(SplitTask{f, i0, k * W, std::min(cmax, (k + 1) * W), slot, nk, k, blk});
+          }
+        }
+      }
+      F.split_level_ptr[l + 1] = (int)st.size();
+      wide.clear();
       F.fwd_level_ptr[l + 1] = (int)ft.size();
       F.fwdn_level_ptr[l + 1] = (int)fn.size();
       F.bwd_level_ptr[l + 1] = (int)bt.size();
+      F.bwdn_level_ptr[l + 1] = (int)bn.size();
     }
     F.fwd_tasks = C.upload(ft.data(), ft.size());
     F.fwdn_tasks = C.upload(fn.data(), fn.size());
+    F.split_tasks = C.upload(st.data(), st.size());
+    F.split_part = C.alloc<double>((size_t)split_slots * 64 + 1);
+    F.split_ticket = C.alloc<unsigned>((size_t)split_blocks + 1);
+    JGS2_CUDA(cudaMemset(F.split_ticket, 0, ((size_t)split_blocks + 1) * sizeof(unsigned)));
     // flat per-level assemble map (forward) and gather map (backward):
     // one entry per front position; contributions in child order.
     std::vector<int64_t> adst, acp(1, 0), asrc, gdst;
@@ -606,6 +820,7 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
     F.gat_dst = C.upload(gdst.data(), gdst.size());
     F.gat_src = C.upload(gsrc.data(), gsrc.size());
     F.bwd_tasks = C.upload(bt.data(), bt.size());
+    F.bwdn_tasks = C.upload(bn.data(), bn.size());
   }
   // ---- device metadata
   F.f_colbeg = C.upload(colbeg.data(), NF);
@@ -794,44 +1009,86 @@ void factor_build(Ctx& C, double h_ref, int leaf, const BlockInput* blocks = nul
 // apply) leave z in b; backward level sweeps (gather + apply) write x into q.
 void factor_solve_launches(Ctx& C) {
   Factor& F = C.fac;
+  // A level's narrow-front launch runs on the side stream beside its wide
+  // launch (disjoint fronts); both join before the next level (captured as
+  // parallel graph branches). The narrow grid fills the wide kernel's tail.
+  const bool fork = solve_fork() && C.solve_side;
+  auto side_begin = [&](bool wide_too) -> cudaStream_t {
+    if (!fork || !wide_too) return C.stream;
+    JGS2_CUDA(cudaEventRecord(C.ev_sfork, C.stream));
+    JGS2_CUDA(cudaStreamWaitEvent(C.solve_side, C.ev_sfork, 0));
+    return C.solve_side;
+  };
+  auto side_end = [&](cudaStream_t s) {
+    if (s == C.stream) return;
+    JGS2_CUDA(cudaEventRecord(C.ev_sjoin, s));
+    JGS2_CUDA(cudaStreamWaitEvent(C.stream, C.ev_sjoin, 0));
+  };
   for (int l = 0; l < F.nlevels; ++l) {
     int64_t na = F.asm_level_ptr[l + 1] - F.asm_level_ptr[l];
     int64_t o = F.asm_level_ptr[l];
     int nt = F.fwd_level_ptr[l + 1] - F.fwd_level_ptr[l];
     int nn = F.fwdn_level_ptr[l + 1] - F.fwdn_level_ptr[l];
-    if (na == 0 && nt == 0 && nn == 0) continue;  // level of zero-size joining fronts
+    int nsp = F.split_level_ptr[l + 1] - F.split_level_ptr[l];
+    if (na == 0 && nt == 0 && nn == 0 && nsp == 0) continue;  // level of zero-size joining fronts
     if (na > 0)
     k_fwd_assemble_flat<<<grid_for(na), kBlock, 0, C.stream>>>(na, F.asm_dst + o, F.asm_b + o,
                                                                F.asm_cp + o, F.asm_src, C.b, F.u, F.w);
     C.check_launch();
+    cudaStream_t sn = C.stream;
     if (nn > 0) {
+      sn = side_begin(nt > 0 || nsp > 0);
       int gn = std::min((nn + 7) / 8, 148 * 8);
-      k_fwd_apply_narrow<<<gn, kSolveThreads, 0, C.stream>>>(F.fwdn_tasks + F.fwdn_level_ptr[l], nn,
-                                                             F.f_colbeg, F.f_ns, F.f_nr, F.f_ld, F.f_loff,
-                                                             F.f_uoff, F.f_woff, F.L, F.w, C.b, F.u);
+      k_fwd_apply_narrow<<<gn, kSolveThreads, 0, sn>>>(F.fwdn_tasks + F.fwdn_level_ptr[l], nn,
+                                                       F.f_colbeg, F.f_ns, F.f_nr, F.f_ld, F.f_loff,
+                                                       F.f_uoff, F.f_woff, F.L, F.w, C.b, F.u);
       C.check_launch();
     }
-    if (nt == 0) continue;
-    int g = std::min(nt, 148 * kApplyCtasPerSm);
-    k_fwd_apply<<<g, kSolveThreads, 0, C.stream>>>(F.fwd_tasks + F.fwd_level_ptr[l], nt, F.f_colbeg,
-                                                   F.f_ns, F.f_nr, F.f_ld, F.f_loff, F.f_uoff,
-                                                   F.f_woff, F.L, F.w, C.b, F.u);
-    C.check_launch();
+    int ns_ = F.split_level_ptr[l + 1] - F.split_level_ptr[l];
+    if (ns_ > 0) {
+      int g = std::min(ns_, 148 * kApplyCtasPerSm);
+      k_fwd_apply_split<<<g, kSolveThreads, 0, C.stream>>>(F.split_tasks + F.split_level_ptr[l], ns_,
+                                                           F.f_colbeg, F.f_ns, F.f_nr, F.f_ld, F.f_loff,
+                                                           F.f_uoff, F.f_woff, F.L, F.w, C.b, F.u,
+                                                           F.split_part, F.split_ticket);
+      C.check_launch();
+    }
+    if (nt > 0) {
+      int g = std::min(nt, 148 * kApplyCtasPerSm);
+      k_fwd_apply<<<g, kSolveThreads, 0, C.stream>>>(F.fwd_tasks + F.fwd_level_ptr[l], nt, F.f_colbeg,
+                                                     F.f_ns, F.f_nr, F.f_ld, F.f_loff, F.f_uoff,
+                                                     F.f_woff, F.L, F.w, C.b, F.u);
+      C.check_launch();
+    }
+    side_end(sn);
   }
   for (int l = F.nlevels - 1; l >= 0; --l) {
     int nt = F.bwd_level_ptr[l + 1] - F.bwd_level_ptr[l];
-    if (nt == 0) continue;
+    int nn = F.bwdn_level_ptr[l + 1] - F.bwdn_level_ptr[l];
+    if (nt == 0 && nn == 0) continue;
     int64_t ng = F.gat_level_ptr[l + 1] - F.gat_level_ptr[l];
     int64_t o = F.gat_level_ptr[l];
     if (ng > 0)
     k_bwd_gather_flat<<<grid_for(ng), kBlock, 0, C.stream>>>(ng, F.gat_dst + o, F.gat_src + o, C.b,
                                                              C.q, F.w);
     C.check_launch();
-    int gb = std::min(nt, 148 * kApplyCtasPerSm);
-    k_bwd_apply<<<gb, kSolveThreads, 0, C.stream>>>(F.bwd_tasks + F.bwd_level_ptr[l], nt, F.f_colbeg,
-                                                    F.f_ns, F.f_nr, F.f_ld, F.f_loff, F.f_woff, F.L,
-                                                    F.w, C.q);
-    C.check_launch();
+    cudaStream_t sn = C.stream;
+    if (nn > 0) {
+      sn = side_begin(nt > 0);
+      int gn = std::min((nn + 7) / 8, 148 * 8);
+      k_bwd_apply_narrow<<<gn, kSolveThreads, 0, sn>>>(F.bwdn_tasks + F.bwdn_level_ptr[l], nn, F.f_colbeg,
+                                                       F.f_ns, F.f_nr, F.f_ld, F.f_loff, F.f_woff, F.L,
+                                                       F.w, C.q);
+      C.check_launch();
+    }
+    if (nt > 0) {
+      int gb = std::min(nt, 148 * kApplyCtasPerSm);
+      k_bwd_apply<<<gb, kSolveThreads, 0, C.stream>>>(F.bwd_tasks + F.bwd_level_ptr[l], nt, F.f_colbeg,
+                                                      F.f_ns, F.f_nr, F.f_ld, F.f_loff, F.f_woff, F.L,
+                                                      F.w, C.q);
+      C.check_launch();
+    }
+    side_end(sn);
   }
 }
 

@@ -41,6 +41,9 @@ jgs2::Ctx::~Ctx() {
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
   if (stream2) cudaStreamDestroy(stream2);
+  if (ev_sfork) cudaEventDestroy(ev_sfork);
+  if (ev_sjoin) cudaEventDestroy(ev_sjoin);
+  if (solve_side) cudaStreamDestroy(solve_side);
   if (fac.graph_exec) cudaGraphExecDestroy(fac.graph_exec);
   delete comm;
   if (stream && own_stream) cudaStreamDestroy(stream);
@@ -655,6 +658,9 @@ jgs2_ctx* jgs2_create(int32_t device) {
     JGS2_CUDA(cudaStreamCreateWithPriority(&C.stream2, cudaStreamNonBlocking, prio_lo));
     JGS2_CUDA(cudaEventCreateWithFlags(&C.ev_fork, cudaEventDisableTiming));
     JGS2_CUDA(cudaEventCreateWithFlags(&C.ev_join, cudaEventDisableTiming));
+    JGS2_CUDA(cudaStreamCreateWithFlags(&C.solve_side, cudaStreamNonBlocking));
+    JGS2_CUDA(cudaEventCreateWithFlags(&C.ev_sfork, cudaEventDisableTiming));
+    JGS2_CUDA(cudaEventCreateWithFlags(&C.ev_sjoin, cudaEventDisableTiming));
     cudaFuncSetAttribute(k_mplus_project, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kProjSmemBytes);
     cudaFuncSetAttribute(k_mplus_full, cudaFuncAttributeMaxDynamicSharedMemorySize,
