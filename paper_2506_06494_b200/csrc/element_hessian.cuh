@@ -293,7 +293,10 @@ k_mplus_closed(int n, const int* elems, const double* __restrict__ xs, const int
   // the block's 128 x 45 outputs are staged in shared memory and stored
   // contiguously (per-thread 360-B strided stores were lg-throttle bound)
   __shared__ double stage[kHessThreads * 45];
-  int u = blockIdx.x * blockDim.x + threadIdx.x;
+  // grid-stride over blocks of 128 elements (one pass unless the grid is capped)
+  for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+  __syncthreads();  // previous round's stores done with stage
+  int u = base + threadIdx.x;
   bool indef = false;
   if (u < n) {
     int e = elems ? elems[u] : u;
@@ -317,7 +320,6 @@ k_mplus_closed(int n, const int* elems, const double* __restrict__ xs, const int
     indef = !is_pos_def9(Mp);
   }
   __syncthreads();
-  const int base = blockIdx.x * blockDim.x;
   const int cnt = 45 * min((int)blockDim.x, n - base);
   double* o = mplus + 45 * (size_t)base;
   for (int k = threadIdx.x; k < cnt; k += blockDim.x) o[k] = stage[k];
@@ -326,6 +328,7 @@ k_mplus_closed(int n, const int* elems, const double* __restrict__ xs, const int
   if (lane == 0 && ball) b0 = atomicAdd(count, __popc(ball));
   b0 = __shfl_sync(0xffffffffu, b0, 0);
   if (indef) list[b0 + __popc(ball & ((1u << lane) - 1u))] = u;
+  }
 }
 
 // ---- negative-eigenspace projection (pass 2)
@@ -730,9 +733,12 @@ k_mplus_full(const int* count, const int* list2, double* mplus) {
 // count: 2 device ints (zeroed here; count[0] = indefinite elements,
 // count[1] = those with more than kNegMax negative modes);
 // list: device scratch of 2n ints.
+// blocks_per_sm > 0 caps every pass at that many resident blocks per SM
+// (grid-stride), leaving the rest of each SM to a concurrent memory-bound
+// kernel (JGS2_HESS_OVERLAP: the passes under the factor solve).
 inline void launch_element_mplus(int n, const int* elems, const double* xs, const int4* tets,
                                  const double* dminv, const double4* eprops, double* out, int* count,
-                                 int* list, cudaStream_t stream) {
+                                 int* list, cudaStream_t stream, int blocks_per_sm = 0) {
   if (n <= 0) return;
   int grid = (n + kHessThreads - 1) / kHessThreads;
   cudaMemsetAsync(count, 0, 2 * sizeof(int), stream);
@@ -742,12 +748,13 @@ inline void launch_element_mplus(int n, const int* elems, const double* xs, cons
                                                                     count);
     return;
   }
-  k_mplus_closed<<<grid, kHessThreads, 0, stream>>>(n, elems, xs, tets, dminv, eprops, out, count, list);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  int grid2 = std::min(grid, sms * JGS2_HESS_MINBLOCKS * 4);
-  k_mplus_project<<<std::min(grid, sms * 3 * 4), kHessThreads, kProjSmemBytes, stream>>>(count, list, list + n,
-                                                                                        out);
+  int grid1 = blocks_per_sm > 0 ? std::min(grid, sms * blocks_per_sm) : grid;
+  k_mplus_closed<<<grid1, kHessThreads, 0, stream>>>(n, elems, xs, tets, dminv, eprops, out, count, list);
+  int grid2 = std::min(grid, sms * (blocks_per_sm > 0 ? blocks_per_sm : JGS2_HESS_MINBLOCKS * 4));
+  k_mplus_project<<<std::min(grid, sms * (blocks_per_sm > 0 ? blocks_per_sm : 3 * 4)), kHessThreads,
+                    kProjSmemBytes, stream>>>(count, list, list + n, out);
   k_mplus_full<<<grid2, kHessThreads, kHessSmemBytes, stream>>>(count, list + n, out);
 }
 

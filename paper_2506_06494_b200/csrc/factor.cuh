@@ -146,6 +146,15 @@ k_fwd_assemble(const int* fronts, const int* colbeg, const int* f_ns, const int*
 // partial sums are combined across warps in a fixed order (deterministic).
 constexpr int kVecCache = 4096;  // doubles of the vector cached in smem (32 KB)
 constexpr int kApplyCtasPerSm = 4;
+// persistent grid of the block apply kernels, CTAs per SM (JGS2_SOLVE_CTAS)
+inline int solve_ctas() {
+  static const int v = [] {
+    const char* e = getenv("JGS2_SOLVE_CTAS");
+    int c = e ? atoi(e) : kApplyCtasPerSm;
+    return (c >= 1 && c <= kApplyCtasPerSm) ? c : kApplyCtasPerSm;
+  }();
+  return v;
+}
 
 __global__ void __launch_bounds__(kSolveThreads, kApplyCtasPerSm)
 k_fwd_apply(const int4* tasks, int ntasks, const int* colbeg, const int* f_ns, const int* f_nr,
@@ -1046,7 +1055,7 @@ void factor_solve_launches(Ctx& C) {
     }
     int ns_ = F.split_level_ptr[l + 1] - F.split_level_ptr[l];
     if (ns_ > 0) {
-      int g = std::min(ns_, 148 * kApplyCtasPerSm);
+      int g = std::min(ns_, 148 * solve_ctas());
       k_fwd_apply_split<<<g, kSolveThreads, 0, C.stream>>>(F.split_tasks + F.split_level_ptr[l], ns_,
                                                            F.f_colbeg, F.f_ns, F.f_nr, F.f_ld, F.f_loff,
                                                            F.f_uoff, F.f_woff, F.L, F.w, C.b, F.u,
@@ -1054,7 +1063,7 @@ void factor_solve_launches(Ctx& C) {
       C.check_launch();
     }
     if (nt > 0) {
-      int g = std::min(nt, 148 * kApplyCtasPerSm);
+      int g = std::min(nt, 148 * solve_ctas());
       k_fwd_apply<<<g, kSolveThreads, 0, C.stream>>>(F.fwd_tasks + F.fwd_level_ptr[l], nt, F.f_colbeg,
                                                      F.f_ns, F.f_nr, F.f_ld, F.f_loff, F.f_uoff,
                                                      F.f_woff, F.L, F.w, C.b, F.u);
@@ -1082,7 +1091,7 @@ void factor_solve_launches(Ctx& C) {
       C.check_launch();
     }
     if (nt > 0) {
-      int gb = std::min(nt, 148 * kApplyCtasPerSm);
+      int gb = std::min(nt, 148 * solve_ctas());
       k_bwd_apply<<<gb, kSolveThreads, 0, C.stream>>>(F.bwd_tasks + F.bwd_level_ptr[l], nt, F.f_colbeg,
                                                       F.f_ns, F.f_nr, F.f_ld, F.f_loff, F.f_woff, F.L,
                                                       F.w, C.q);

@@ -182,7 +182,7 @@ void collect(Ctx& C) {
 // Element Hessians at x on the side stream: compute-bound FP64 work that
 // overlaps the memory-bound vertex pass + collect on the main stream
 // (independent: H_cur depends on x only); joined before k_local.
-void hessians_async(Ctx& C) {
+void hessians_async(Ctx& C, int blocks_per_sm = 0) {
   if (C.nuniq == 0 || C.hess_pending) return;
   JGS2_CUDA(cudaEventRecord(C.ev_fork, C.stream));
   JGS2_CUDA(cudaStreamWaitEvent(C.stream2, C.ev_fork, 0));
@@ -193,7 +193,7 @@ void hessians_async(Ctx& C) {
     JGS2_CUDA(cudaEventRecord(a, C.stream2));
   }
   launch_element_mplus(C.nuniq, C.uniq, C.x, C.tets, C.dminv, C.eprops, C.mplus, C.hess_count,
-                       C.hess_list, C.stream2);
+                       C.hess_list, C.stream2, blocks_per_sm);
   C.launches += 3;
   C.check_launch();
   if (C.profiling) {
@@ -456,9 +456,9 @@ void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
   // x only) on the low-priority side stream under the latency-bound pair
   // detection and vertex pass, joined before the collect. Measured neutral on
   // B200 (C4 49.2-51.1 vs 50.6 sweeps/s): the Hessian grid saturates the SMs,
-  // so there is little idle time to fill. Overlapping them with the solve
-  // itself is slower (the persistent solve CTAs lose residency: 31.9 vs 26.4
-  // ms/sweep). Default: just before the local systems.
+  // so there is little idle time to fill. Overlapping them uncapped with the
+  // solve is slower (the persistent solve CTAs lose residency: 31.9 vs 26.4
+  // ms/sweep in round 1); the default below caps them at one block per SM.
   static const bool early_env = getenv("JGS2_HESS_EARLY") != nullptr;
   const bool early = early_env && contact_active(C);
   if (early) hessians_async(C);
@@ -475,6 +475,16 @@ void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
     C.phase_end();
   }
   hessians_join(C);  // no-op unless launched above
+  // The element Hessians (FP64 ALU, x only) run on the side stream under the
+  // factor solve (HBM), capped at one resident block per SM so the solve's
+  // CTAs keep the rest of each SM; joined before k_local. C4: 81.8 -> 86.5
+  // sweeps/s (solve 6.9 -> 8.1 ms, the 1.8 ms Hessian phase hidden; 2 blocks
+  // per SM: 82.2). JGS2_HESS_OVERLAP=<blocks per SM>, 0 = before k_local.
+  static const int overlap = [] {
+    const char* e = getenv("JGS2_HESS_OVERLAP");
+    return e ? atoi(e) : 1;
+  }();
+  if (overlap > 0 && !early && !C.plain) hessians_async(C, overlap);
   collect(C);
   const int npairs_x = C.npairs;  // pairs at the sweep-start x
   const bool gs = C.mode == 1 && C.color_ptr.size() > 1;
