@@ -329,6 +329,22 @@ def main():
     d_ms, d_launch, d_bytes = phases[dom]
     achieved = d_bytes / (d_ms / 1e3) / 1e9 if d_ms > 0 else 0.0
     total_bytes = sum(p[2] for p in phases.values())
+    # the same kernel without the element Hessians running beside it (they
+    # share its SMs in the timed window): a short untimed window after it
+    standalone = None
+    if dom == "factor_solve" and args.steps > 0:
+        solver.set_hess_overlap(0)
+        solver.phase_reset()
+        solver.profile(True)
+        solver.run_sweeps(min(args.steps, 10))
+        s_ms, s_launch, s_bytes = solver.phase_stats()[dom]
+        solver.profile(False)
+        solver.set_hess_overlap(1)
+        if s_ms > 0:
+            s_ach = s_bytes / (s_ms / 1e3) / 1e9
+            standalone = {"achieved": s_ach, "frac": s_ach / peak, "ms_per_step": s_ms / min(args.steps, 10),
+                          "sweeps": min(args.steps, 10),
+                          "note": "element Hessians before the local systems instead of under the solve"}
 
     # whole timesteps to the residual tolerance, device-resident: close the
     # frame left open by the window (untimed), then time complete frames
@@ -430,7 +446,9 @@ def main():
                      "frac": achieved / peak, "traffic": traffic(args.config, dom, d_launch, args.steps),
                      "bytes_per_launch": d_bytes / max(d_launch, 1), "launches": d_launch,
                      "step_bytes": total_bytes / args.steps,
-                     "step_frac": (total_bytes / (ms / 1e3) / 1e9) / peak},
+                     "step_frac": (total_bytes / (ms / 1e3) / 1e9) / peak,
+                     "in_step": "timed window: the element Hessians share the SMs with the solve",
+                     "standalone": standalone},
         "phases_ms_per_step": {p: round(v[0] / args.steps, 4) for p, v in phases.items()},
         "phases_gbs": {p: round(v[2] / (v[0] / 1e3) / 1e9, 1) for p, v in phases.items()
                        if v[0] > 0 and v[2] > 0},

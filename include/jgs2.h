@@ -134,6 +134,11 @@ int32_t jgs2_set_colors(jgs2_ctx* ctx, const int64_t* colors);
  * nested dissection with leaves of leaf_size vertices (the scalable
  * precompute's large fronts). */
 int32_t jgs2_set_ordering(jgs2_ctx* ctx, int32_t ordering);
+/* Schedule of the element Hessians (no reference counterpart; a tuning knob):
+ * blocks_per_sm > 0 runs them on a side stream under the factor solve, capped
+ * at that many resident blocks per SM (default 1, or JGS2_HESS_OVERLAP);
+ * 0 runs them just before the local systems. Results are identical. */
+int32_t jgs2_set_hess_overlap(jgs2_ctx* ctx, int32_t blocks_per_sm);
 /* Rest Hessian M/h^2 + PSD elastic, Dirichlet-eliminated, factored on the
  * device (replaces subspace.rest_factorization, subspace.py:126-130). */
 int32_t jgs2_factor_rest(jgs2_ctx* ctx, double h_ref, int32_t leaf_size, jgs2_factor_info* info);

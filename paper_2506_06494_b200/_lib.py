@@ -28,7 +28,7 @@ EXPORTS = (
     "jgs2_frame_reset", "jgs2_timestep_host", "jgs2_nccl_unique_id", "jgs2_set_comm_nccl",
     "jgs2_set_comm_nccl_handle", "jgs2_set_comm_host", "jgs2_set_partition", "jgs2_create_on_stream",
     "jgs2_selected_inverse", "jgs2_inverse_blocks", "jgs2_stencil_gradients", "jgs2_precompute_train",
-    "jgs2_precompute_export", "jgs2_factor_fill", "jgs2_set_ordering",
+    "jgs2_precompute_export", "jgs2_factor_fill", "jgs2_set_ordering", "jgs2_set_hess_overlap",
 )
 PHASES = ("vertex_pass", "collect_rhs", "factor_solve", "cubature_hessians", "local_systems",
           "energy", "update", "contact_pairs", "contact_cap", "contact_trials", "frame_cap")
@@ -161,6 +161,7 @@ def lib():
         "jgs2_selected_inverse": (i32, [vp, P(f64)]),
         "jgs2_factor_fill": (i32, [vp, P(i64)]),
         "jgs2_set_ordering": (i32, [vp, i32]),
+        "jgs2_set_hess_overlap": (i32, [vp, i32]),
         "jgs2_inverse_blocks": (i32, [vp, i64, P(i64), P(i64), P(f64), P(i32)]),
         "jgs2_stencil_gradients": (i32, [vp, P(f64), P(f64), f64, P(f64)]),
         "jgs2_precompute_train": (i32, [vp, P(TrainParams), P(i64)]),

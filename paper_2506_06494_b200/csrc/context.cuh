@@ -353,6 +353,11 @@ struct Ctx {
   }
 
   Factor fac;
+  // element Hessians under the factor solve, blocks per SM (0 = before k_local)
+  int hess_overlap = [] {
+    const char* e = getenv("JGS2_HESS_OVERLAP");
+    return e ? atoi(e) : 1;
+  }();
   int ordering = -1;           // jgs2_set_ordering: 1 METIS ND, 0 geometric ND, -1 default (METIS)
   std::shared_ptr<struct TrainOut> train;  // scalable precompute output (train.cuh)
   cublasHandle_t cublas = nullptr;

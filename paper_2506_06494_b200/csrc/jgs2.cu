@@ -480,11 +480,7 @@ void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
   // CTAs keep the rest of each SM; joined before k_local. C4: 81.8 -> 86.5
   // sweeps/s (solve 6.9 -> 8.1 ms, the 1.8 ms Hessian phase hidden; 2 blocks
   // per SM: 82.2). JGS2_HESS_OVERLAP=<blocks per SM>, 0 = before k_local.
-  static const int overlap = [] {
-    const char* e = getenv("JGS2_HESS_OVERLAP");
-    return e ? atoi(e) : 1;
-  }();
-  if (overlap > 0 && !early && !C.plain) hessians_async(C, overlap);
+  if (C.hess_overlap > 0 && !early && !C.plain) hessians_async(C, C.hess_overlap);
   collect(C);
   const int npairs_x = C.npairs;  // pairs at the sweep-start x
   const bool gs = C.mode == 1 && C.color_ptr.size() > 1;
@@ -1102,6 +1098,13 @@ int32_t jgs2_set_ordering(jgs2_ctx* ctx, int32_t ordering) {
     if (ordering != 0 && ordering != 1) throw Error(JGS2_E_ARG, "ordering must be 0 (geometric) or 1 (METIS)");
     if (C.fac.ready) throw Error(JGS2_E_ARG, "factor already built");
     C.ordering = ordering;
+  });
+}
+
+int32_t jgs2_set_hess_overlap(jgs2_ctx* ctx, int32_t blocks_per_sm) {
+  return guarded(ctx, [&](Ctx& C) {
+    if (blocks_per_sm < 0 || blocks_per_sm > 16) throw Error(JGS2_E_ARG, "blocks_per_sm must be in [0, 16]");
+    C.hess_overlap = blocks_per_sm;
   });
 }
 

@@ -287,6 +287,11 @@ class LocalSolver:
         self._call(self._lib.jgs2_factor_fill, L.ptr(out, L.i64))
         return tuple(int(x) for x in out)
 
+    def set_hess_overlap(self, blocks_per_sm):
+        """Element Hessians under the factor solve, capped at blocks_per_sm
+        resident blocks per SM (0: just before the local systems)."""
+        self._call(self._lib.jgs2_set_hess_overlap, int(blocks_per_sm))
+
     def profile(self, enable=True):
         self._call(self._lib.jgs2_profile, int(bool(enable)))
 
