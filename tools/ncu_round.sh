@@ -11,7 +11,11 @@ ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.s
     --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py $ARGS > gpurun_out/${TAG}_ncu_list.log 2>&1
 python profiles/parse_launches.py gpurun_out/${TAG}_launches.csv > gpurun_out/${TAG}_c4_launches.txt
 head -25 gpurun_out/${TAG}_c4_launches.txt
-ncu --kernel-name regex:"k_fwd_apply$|k_local|k_mplus_project|k_vertex_pass" --launch-skip 20 --launch-count 4 \
+ncu --kernel-name regex:"${NCU_FULL_RE:-k_fwd_apply$|k_local|k_mplus_project|k_vertex_pass}" \
+    --launch-skip ${NCU_FULL_SKIP:-20} --launch-count ${NCU_FULL_COUNT:-4} \
     --set full --import-source on --clock-control none -o gpurun_out/${TAG}_full python bench.py $ARGS \
     > gpurun_out/${TAG}_ncu_full.log 2>&1
 tail -2 gpurun_out/${TAG}_ncu_full.log
+# per-kernel details as CSV (the .ncu-rep stays out of gpurun_out: 64 MiB cap)
+ncu -i gpurun_out/${TAG}_full.ncu-rep --page details --csv > gpurun_out/${TAG}_full_details.csv 2>&1 || true
+rm -f gpurun_out/${TAG}_full.ncu-rep
