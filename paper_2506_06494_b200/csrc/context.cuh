@@ -216,6 +216,12 @@ struct Ctx {
   cudaStream_t stream2 = nullptr;  // side stream for the element-Hessian passes
   cudaStream_t solve_side = nullptr;  // factor solve: a level's narrow launches beside the wide ones
   cudaEvent_t ev_sfork = nullptr, ev_sjoin = nullptr;
+  cudaStream_t vp_stream = nullptr;  // vertex pass under the pair detection
+  cudaEvent_t ev_vfork = nullptr, ev_vjoin = nullptr;
+  bool vp_overlap = [] {
+    const char* e = getenv("JGS2_VP_OVERLAP");
+    return !(e && e[0] == '0');
+  }();
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool hess_pending = false;
   // retained rows CSR for contact coupling rows (local_solver.py:85-112)

@@ -44,6 +44,10 @@ jgs2::Ctx::~Ctx() {
   if (ev_sfork) cudaEventDestroy(ev_sfork);
   if (ev_sjoin) cudaEventDestroy(ev_sjoin);
   if (solve_side) cudaStreamDestroy(solve_side);
+  if (vp_stream) cudaStreamSynchronize(vp_stream);
+  if (ev_vfork) cudaEventDestroy(ev_vfork);
+  if (ev_vjoin) cudaEventDestroy(ev_vjoin);
+  if (vp_stream) cudaStreamDestroy(vp_stream);
   if (fac.graph_exec) cudaGraphExecDestroy(fac.graph_exec);
   delete comm;
   if (stream && own_stream) cudaStreamDestroy(stream);
@@ -146,6 +150,35 @@ void vertex_pass(Ctx& C, bool rot) {
   C.phase_end();
   if (rot) C.rot_valid = true;
 }
+
+// The vertex pass on a side stream under the pair detection (both read x
+// only; the detection is latency bound with host syncs for its counts):
+// joined before the pair gradients are added to g_asm.
+void vertex_pass_async(Ctx& C, bool rot) {
+  DevModel m = devmodel(C);
+  JGS2_CUDA(cudaEventRecord(C.ev_vfork, C.stream));
+  JGS2_CUDA(cudaStreamWaitEvent(C.vp_stream, C.ev_vfork, 0));
+  C.phase_bytes[0] += bytes_vertex(C);
+  cudaEvent_t a = nullptr;
+  if (C.profiling) {
+    a = C.take_event();
+    JGS2_CUDA(cudaEventRecord(a, C.vp_stream));
+  }
+  int nown = C.own_v1 - C.own_v0;
+  if (rot) k_vertex_pass<true><<<grid_for(nown), kBlock, 0, C.vp_stream>>>(m, C.x, C.z, C.h, C.R, C.gasm);
+  else k_vertex_pass<false><<<grid_for(nown), kBlock, 0, C.vp_stream>>>(m, C.x, C.z, C.h, C.R, C.gasm);
+  C.check_launch();
+  if (C.profiling) {
+    cudaEvent_t b = C.take_event();
+    JGS2_CUDA(cudaEventRecord(b, C.vp_stream));
+    C.phase_launch[0] += 1;
+    C.pending.push_back({0, {a, b}});
+  }
+  JGS2_CUDA(cudaEventRecord(C.ev_vjoin, C.vp_stream));
+  if (rot) C.rot_valid = true;
+}
+
+void vertex_pass_join(Ctx& C) { JGS2_CUDA(cudaStreamWaitEvent(C.stream, C.ev_vjoin, 0)); }
 
 // grad_sq over the free vertices (local_solver.py:602-603) in vertex chunks:
 // this rank's chunks, all-reduced, combined in chunk order into res[R_GRADSQ]
@@ -462,13 +495,16 @@ void sweep_core(Ctx& C, bool rot, jgs2_sweep_info* info) {
   static const bool early_env = getenv("JGS2_HESS_EARLY") != nullptr;
   const bool early = early_env && contact_active(C);
   if (early) hessians_async(C);
+  const bool vp_async = C.vp_overlap && contact_active(C);
+  if (vp_async) vertex_pass_async(C, rot);
   if (contact_active(C)) {  // pairs at x (local_solver.py:612)
     C.phase_begin(7, 0.0);
     contact_find_pairs(C, C.x, nullptr, 0.0);
     C.phase_end();
+    if (vp_async) vertex_pass_join(C);
     if (contact_infeasible(C)) throw Error(JGS2_E_INFEASIBLE, "barrier distance <= 0 at the sweep start");
   }
-  vertex_pass(C, rot);
+  if (!vp_async) vertex_pass(C, rot);
   if (contact_active(C)) {
     C.phase_begin(7, 0.0);
     contact_add_gradients(C);
@@ -665,6 +701,9 @@ jgs2_ctx* jgs2_create(int32_t device) {
     JGS2_CUDA(cudaEventCreateWithFlags(&C.ev_fork, cudaEventDisableTiming));
     JGS2_CUDA(cudaEventCreateWithFlags(&C.ev_join, cudaEventDisableTiming));
     JGS2_CUDA(cudaStreamCreateWithFlags(&C.solve_side, cudaStreamNonBlocking));
+    JGS2_CUDA(cudaStreamCreateWithFlags(&C.vp_stream, cudaStreamNonBlocking));
+    JGS2_CUDA(cudaEventCreateWithFlags(&C.ev_vfork, cudaEventDisableTiming));
+    JGS2_CUDA(cudaEventCreateWithFlags(&C.ev_vjoin, cudaEventDisableTiming));
     JGS2_CUDA(cudaEventCreateWithFlags(&C.ev_sfork, cudaEventDisableTiming));
     JGS2_CUDA(cudaEventCreateWithFlags(&C.ev_sjoin, cudaEventDisableTiming));
     cudaFuncSetAttribute(k_mplus_project, cudaFuncAttributeMaxDynamicSharedMemorySize,
