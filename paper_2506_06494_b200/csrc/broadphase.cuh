@@ -29,17 +29,25 @@ __device__ __forceinline__ long long cell_coord(double v, double inv_cell) {
   c = c < -kCellOff + 1 ? -kCellOff + 1 : (c > kCellOff - 2 ? kCellOff - 2 : c);
   return c;
 }
-__device__ __forceinline__ unsigned long long cell_key(long long ix, long long iy, long long iz) {
-  return ((unsigned long long)(ix + kCellOff) << 42) | ((unsigned long long)(iy + kCellOff) << 21) |
-         (unsigned long long)(iz + kCellOff);
-}
 
+// Cell keys are packed relative to the bounding box of all triangle cells
+// (k_grid_count reduces it): key = (ix-X0) << (by+bz) | (iy-Y0) << bz | (iz-Z0),
+// so the radix sort covers bx+by+bz bits (about 24-30 at C4) instead of 63.
+// The key order across cells is irrelevant to the lookups; within a cell the
+// stable sort keeps the entries in ascending triangle id.
 struct TriGridDev {
   const unsigned long long* keys;  // sorted cell keys
   const int* tris;                 // triangle ids, ascending within a key
   long long n;
   double inv_cell;
+  long long x0, y0, z0, x1, y1, z1;  // cell bounding box (inclusive)
+  int sy, sz;                        // shifts of the x and y fields
 };
+
+__device__ __forceinline__ unsigned long long box_key(const TriGridDev& g, long long i, long long j, long long k) {
+  return ((unsigned long long)(i - g.x0) << g.sy) | ((unsigned long long)(j - g.y0) << g.sz) |
+         (unsigned long long)(k - g.z0);
+}
 
 __device__ __forceinline__ void tri_bounds(const int* st, int t, const double* x, const double* dx,
                                            double gamma, double r, double inv_cell, long long* lo,
@@ -57,20 +65,49 @@ __device__ __forceinline__ void tri_bounds(const int* st, int t, const double* x
   }
 }
 
+__global__ void k_box_init(long long* box) {
+  if (threadIdx.x < 3) box[threadIdx.x] = LLONG_MAX;
+  else if (threadIdx.x < 6) box[threadIdx.x] = LLONG_MIN;
+}
+
+// entries per triangle, and the cell bounding box of all triangles (box:
+// min x y z, max x y z; block-reduced, then one atomic per block and bound)
 __global__ void k_grid_count(int nst, const int* st, const double* x, const double* dx, double gamma,
-                             double r, double inv_cell, long long* counts) {
+                             double r, double inv_cell, long long* counts, long long* box) {
+  __shared__ long long sb[6][kBlock / 32];
   int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t > nst) return;
-  if (t == nst) { counts[t] = 0; return; }
-  long long lo[3], hi[3];
-  tri_bounds(st, t, x, dx, gamma, r, inv_cell, lo, hi);
-  long long c = (hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1) * (hi[2] - lo[2] + 1);
-  counts[t] = (c > 0 && c < (1LL << 20)) ? c : (1LL << 40);  // flags garbage (NaN) bounds
+  long long lo[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX}, hi[3] = {LLONG_MIN, LLONG_MIN, LLONG_MIN};
+  if (t < nst) {
+    tri_bounds(st, t, x, dx, gamma, r, inv_cell, lo, hi);
+    long long c = (hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1) * (hi[2] - lo[2] + 1);
+    counts[t] = (c > 0 && c < (1LL << 20)) ? c : (1LL << 40);  // flags garbage (NaN) bounds
+  } else if (t == nst) {
+    counts[t] = 0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = min(lo[a], __shfl_down_sync(0xffffffffu, lo[a], o));
+      hi[a] = max(hi[a], __shfl_down_sync(0xffffffffu, hi[a], o));
+    }
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0)
+    for (int a = 0; a < 3; ++a) { sb[a][w] = lo[a]; sb[3 + a][w] = hi[a]; }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    long long v = sb[threadIdx.x][0];
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k)
+      v = threadIdx.x < 3 ? min(v, sb[threadIdx.x][k]) : max(v, sb[threadIdx.x][k]);
+    if (threadIdx.x < 3) { if (v != LLONG_MAX) atomicMin(box + threadIdx.x, v); }
+    else if (v != LLONG_MIN) atomicMax(box + threadIdx.x, v);
+  }
 }
 
 __global__ void k_grid_write(int nst, const int* st, const double* x, const double* dx, double gamma,
-                             double r, double inv_cell, const long long* off, unsigned long long* keys,
+                             double r, TriGridDev g, const long long* off, unsigned long long* keys,
                              int* tris) {
+  const double inv_cell = g.inv_cell;
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nst) return;
   long long lo[3], hi[3];
@@ -80,7 +117,7 @@ __global__ void k_grid_write(int nst, const int* st, const double* x, const doub
   for (long long i = lo[0]; i <= hi[0]; ++i)
     for (long long j = lo[1]; j <= hi[1]; ++j)
       for (long long k = lo[2]; k <= hi[2]; ++k) {
-        keys[o] = cell_key(i, j, k);
+        keys[o] = box_key(g, i, j, k);
         tris[o] = t;
         ++o;
       }
@@ -129,17 +166,24 @@ __device__ __forceinline__ void visit_cross(long long q0, long long q1, int bv, 
   for (long long q = o1; q < q1; ++q) visit(q);
 }
 
-__device__ __forceinline__ unsigned long long point_key(const double* p, double inv_cell) {
-  return cell_key(cell_coord(p[0], inv_cell), cell_coord(p[1], inv_cell), cell_coord(p[2], inv_cell));
+// the key of p's cell, or ~0 (matches no entry) outside the triangles' box
+__device__ __forceinline__ unsigned long long point_key(const TriGridDev& g, const double* p) {
+  long long i = cell_coord(p[0], g.inv_cell), j = cell_coord(p[1], g.inv_cell), k = cell_coord(p[2], g.inv_cell);
+  if (i < g.x0 || i > g.x1 || j < g.y0 || j > g.y1 || k < g.z0 || k > g.z1) return ~0ULL;
+  return box_key(g, i, j, k);
 }
 
 inline TriGridDev grid_dev(const TriGrid& g) {
-  return TriGridDev{g.keys_b, g.tris_b, g.n, 1.0 / g.cell};
+  TriGridDev d{g.keys_b, g.tris_b, g.n, 1.0 / g.cell};
+  d.x0 = g.box[0]; d.y0 = g.box[1]; d.z0 = g.box[2];
+  d.x1 = g.box[3]; d.y1 = g.box[4]; d.z1 = g.box[5];
+  d.sy = g.sy; d.sz = g.sz;
+  return d;
 }
 
 inline void tri_grid_free(TriGrid& g) {
   cudaFree(g.counts); cudaFree(g.off); cudaFree(g.keys_a); cudaFree(g.keys_b);
-  cudaFree(g.tris_a); cudaFree(g.tris_b); cudaFree(g.temp);
+  cudaFree(g.tris_a); cudaFree(g.tris_b); cudaFree(g.temp); cudaFree(g.dbox);
   g = TriGrid();
 }
 
@@ -153,7 +197,11 @@ inline void tri_grid_build(Ctx& C, TriGrid& g, const double* x, const double* dx
     JGS2_CUDA(cudaMalloc(&g.counts, (nst + 1) * sizeof(long long)));
     JGS2_CUDA(cudaMalloc(&g.off, (nst + 1) * sizeof(long long)));
   }
-  k_grid_count<<<grid_for(nst + 1), kBlock, 0, C.stream>>>(nst, C.st, x, dx, gamma, r, 1.0 / cell, g.counts);
+  if (!g.dbox) JGS2_CUDA(cudaMalloc(&g.dbox, 6 * sizeof(long long)));
+  k_box_init<<<1, 32, 0, C.stream>>>(g.dbox);
+  C.check_launch();
+  k_grid_count<<<grid_for(nst + 1), kBlock, 0, C.stream>>>(nst, C.st, x, dx, gamma, r, 1.0 / cell, g.counts,
+                                                           g.dbox);
   C.check_launch();
   size_t tb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tb, g.counts, g.off, nst + 1, C.stream);
@@ -168,6 +216,7 @@ inline void tri_grid_build(Ctx& C, TriGrid& g, const double* x, const double* dx
   static const bool dbg = getenv("JGS2_DEBUG_PAIRS") != nullptr;
   auto tq = std::chrono::steady_clock::now();
   JGS2_CUDA(cudaMemcpyAsync(&total, g.off + nst, sizeof(long long), cudaMemcpyDeviceToHost, C.stream));
+  JGS2_CUDA(cudaMemcpyAsync(g.box, g.dbox, 6 * sizeof(long long), cudaMemcpyDeviceToHost, C.stream));
   C.sync();
   if (dbg) {
     double w = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tq).count();
@@ -186,11 +235,24 @@ inline void tri_grid_build(Ctx& C, TriGrid& g, const double* x, const double* dx
     g.cap = cap;
   }
   g.n = total;
-  k_grid_write<<<grid_for(nst), kBlock, 0, C.stream>>>(nst, C.st, x, dx, gamma, r, 1.0 / cell, g.off, g.keys_a,
+  auto bits_for = [](long long n) { int b = 0; while (b < 62 && (1LL << b) < n) ++b; return b; };
+  int bx = 1, by = 1, bz = 1;
+  if (total > 0) {
+    bx = std::max(1, bits_for(g.box[3] - g.box[0] + 1));
+    by = std::max(1, bits_for(g.box[4] - g.box[1] + 1));
+    bz = std::max(1, bits_for(g.box[5] - g.box[2] + 1));
+  } else {
+    for (int a = 0; a < 3; ++a) { g.box[a] = 0; g.box[3 + a] = -1; }  // empty box: no query matches
+  }
+  if (bx + by + bz > 63) throw Error(-2, "broadphase: cell box too large for 63-bit keys");
+  g.sz = bz;
+  g.sy = by + bz;
+  const int end_bit = bx + by + bz;
+  k_grid_write<<<grid_for(nst), kBlock, 0, C.stream>>>(nst, C.st, x, dx, gamma, r, grid_dev(g), g.off, g.keys_a,
                                                        g.tris_a);
   C.check_launch();
   size_t sb = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, sb, g.keys_a, g.keys_b, g.tris_a, g.tris_b, (int)total, 0, 63,
+  cub::DeviceRadixSort::SortPairs(nullptr, sb, g.keys_a, g.keys_b, g.tris_a, g.tris_b, (int)total, 0, end_bit,
                                   C.stream);
   if (sb > g.temp_bytes) {  // the sort's scratch grows with the entry count: 1.5x slack
     cudaFree(g.temp);
@@ -198,7 +260,7 @@ inline void tri_grid_build(Ctx& C, TriGrid& g, const double* x, const double* dx
     g.temp_bytes = sb + sb / 2;
   }
   JGS2_CUDA(cub::DeviceRadixSort::SortPairs(g.temp, sb, g.keys_a, g.keys_b, g.tris_a, g.tris_b, (int)total,
-                                            0, 63, C.stream));
+                                            0, end_bit, C.stream));
   ++C.launches;
   if (dbg) {
     auto ts = std::chrono::steady_clock::now();

@@ -50,7 +50,7 @@ __global__ void k_pair_count(ContactDev cd, TriGridDev g, int use_grid, const do
   };
   if (use_grid) {
     long long q0, q1;
-    grid_range(g, point_key(p, g.inv_cell), &q0, &q1);
+    grid_range(g, point_key(g, p), &q0, &q1);
     visit_cross(q0, q1, bv, [&](long long q) { return cd.tbody[g.tris[q]]; },
                 [&](long long q) { test(g.tris[q]); });
   } else {
@@ -99,7 +99,7 @@ __global__ void k_pair_write(ContactDev cd, TriGridDev g, int use_grid, const do
   };
   if (use_grid) {
     long long q0, q1;
-    grid_range(g, point_key(p, g.inv_cell), &q0, &q1);
+    grid_range(g, point_key(g, p), &q0, &q1);
     visit_cross(q0, q1, bv, [&](long long q) { return cd.tbody[g.tris[q]]; },
                 [&](long long q) { emit(g.tris[q]); });
   } else {
@@ -589,7 +589,7 @@ void contact_find_pairs(Ctx& C, const double* x, const double* dx, double gamma)
   int n = (C.nplanes + 1) * C.nsv;
   JGS2_CUDA(cudaMemsetAsync(C.flag_d, 0, sizeof(int), C.stream));
   int ug = use_tri_grid(C) ? 1 : 0;
-  TriGridDev gd{nullptr, nullptr, 0, 1.0};
+  TriGridDev gd{nullptr, nullptr, 0, 1.0, 0, 0, 0, -1, -1, -1, 0, 0};
   static const bool dbg = getenv("JGS2_DEBUG_PAIRS") != nullptr;
   using clk = std::chrono::steady_clock;
   auto ms = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };

@@ -54,6 +54,9 @@ struct TriGrid {
   void* temp = nullptr;
   size_t temp_bytes = 0;
   double cell = 0.0;
+  long long* dbox = nullptr;  // device cell bounding box (min xyz, max xyz)
+  long long box[6] = {0, 0, 0, -1, -1, -1};
+  int sy = 0, sz = 0;         // key shifts (broadphase.cuh)
 };
 
 // Sorted (key, id) entry list of the hierarchical cap grids (hier_grid.cuh).
