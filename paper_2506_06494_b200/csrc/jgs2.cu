@@ -65,6 +65,18 @@ namespace {
 template <class F>
 int32_t guarded(jgs2_ctx* ctx, F&& fn) {
   if (!ctx) return JGS2_E_ARG;
+  // a call that threw between a side-stream fork and its join (element
+  // Hessians under the solve, vertex pass under the pair detection) leaves
+  // that work in flight: order it before anything later on the main stream,
+  // and never let a later sweep join the stale Hessians as its own
+  auto settle = [](Ctx& C) {
+    if (C.hess_pending) {
+      if (C.ev_join) cudaStreamWaitEvent(C.stream, C.ev_join, 0);
+      C.hess_pending = false;
+    }
+    if (C.ev_vjoin) cudaStreamWaitEvent(C.stream, C.ev_vjoin, 0);
+    cudaGetLastError();
+  };
   try {
     ctx->c.err.clear();
     JGS2_CUDA(cudaSetDevice(ctx->c.device));
@@ -72,9 +84,11 @@ int32_t guarded(jgs2_ctx* ctx, F&& fn) {
     return JGS2_OK;
   } catch (const Error& e) {
     ctx->c.err = e.what();
+    settle(ctx->c);
     return e.code;
   } catch (const std::exception& e) {
     ctx->c.err = e.what();
+    settle(ctx->c);
     return JGS2_E_ARG;
   }
 }
