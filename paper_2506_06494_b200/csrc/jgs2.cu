@@ -706,6 +706,7 @@ jgs2_ctx* jgs2_create(int32_t device) {
   int prio_lo = 0, prio_hi = 0;
   if (cudaSetDevice(device) != cudaSuccess || cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi) != cudaSuccess ||
       cudaStreamCreateWithPriority(&ctx->c.stream, cudaStreamNonBlocking, prio_hi) != cudaSuccess) {
+    fprintf(stderr, "jgs2_create: %s\n", cudaGetErrorString(cudaGetLastError()));
     delete ctx;
     return nullptr;
   }
@@ -737,7 +738,8 @@ jgs2_ctx* jgs2_create(int32_t device) {
     cudaFuncSetAttribute(k_element_mplus, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kHessSmemBytes);
 
-  } catch (...) {
+  } catch (const std::exception& e) {
+    fprintf(stderr, "jgs2_create: %s\n", e.what());
     delete ctx;
     return nullptr;
   }
