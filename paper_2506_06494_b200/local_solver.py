@@ -138,6 +138,14 @@ def matrix_blocks(hbar):
     return rows, b.indices.astype(np.int64), np.ascontiguousarray(b.data, dtype=np.float64)
 
 
+def _require_finite(*arrays):
+    """Non-finite positions are rejected on the host: on the device they end
+    in an illegal memory access that poisons the context."""
+    for a in arrays:
+        if not np.isfinite(a).all():
+            raise ValueError("non-finite positions (NaN or inf) in the state")
+
+
 class LocalSolver:
     """GPU JGS2 solver with the reference ``LocalSolver`` interface.
 
@@ -369,6 +377,7 @@ class LocalSolver:
             rotations = np.broadcast_to(np.eye(3), (self.nv, 3, 3))
         x = L.f64a(state.x)
         z = L.f64a(state.z)
+        _require_finite(x, z)
         rot = L.f64a(rotations)
         x_out = np.empty_like(x)
         dx = np.empty_like(x)
@@ -391,6 +400,7 @@ class LocalSolver:
         cfg = self.config
         stats = IterationStats()
         t0 = time.perf_counter()
+        _require_finite(state.x, state.z)
         self.set_state(state.x, state.z, state.h)
         for _ in range(cfg.max_outer):
             t1 = time.perf_counter()

@@ -245,6 +245,32 @@ def test_gauss_seidel_penetration_raises_like_reference():
     pytest.skip("no penetration within 3 sweeps")
 
 
+def test_nonfinite_state_rejected_and_solver_unharmed():
+    # NaN positions raise ValueError on the host (on the device they would
+    # poison the context); the solver's next sweep equals a fresh solver's
+    from paper_2506_06494_b200 import scenes
+    from paper_2506_06494_b200.model import SystemState
+    from paper_2506_06494_b200.precompute import Precompute
+    m, st, h, _ = scenes.build("c4s6")
+    pre = Precompute.injected(m, h, samples=6, seed=0)
+    cp = lambda: SystemState(x=st.x.copy(), x_prev=st.x_prev.copy(), v=st.v.copy(),  # noqa: E731
+                             z=st.z.copy(), h=h)
+    cfg = SolverConfig(tol_dx=m.tol_dx)
+    s = LocalSolver(m, cfg, precompute=pre, h_ref=h)
+    bad = cp()
+    bad.x[5] = np.nan
+    with pytest.raises(ValueError):
+        s.sweep(bad)
+    with pytest.raises(ValueError):
+        s.outer_solve(bad)
+    s2 = LocalSolver(m, cfg, precompute=pre, h_ref=h)
+    a, b = cp(), cp()
+    dxa, _ = s.sweep(a, s.rotations(a.x))
+    dxb, _ = s2.sweep(b, s2.rotations(b.x))
+    assert np.array_equal(a.x, b.x)
+    assert np.array_equal(dxa, dxb)
+
+
 def test_run_frames_from_reference_cache_matches_reference(golden, tmp_path):
     # harness.run-style frames on the GPU solver, precompute loaded from the
     # cache files the reference wrote; outputs in the reference's formats
